@@ -1,0 +1,217 @@
+"""Pins of the oracle NFFT (oracle/nfft.py) and NDFT (oracle/ndft.py).
+
+Each test checks the oracle against something other than itself: the exact
+NDFT by brute force, a library FFT on a special case, exact rational
+arithmetic, closed forms, or an invariant of the mathematics.
+"""
+
+import fractions
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ndft, nfft
+from paper_2208_00049_b200 import workloads
+from conftest import rel_inf, rel_l2
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _rand(seed, M, N):
+    rng = np.random.default_rng(seed)
+    nodes = workloads.uniform_nodes(rng, M, len(N))
+    fhat = workloads.complex_normal(rng, tuple(N))
+    f = workloads.complex_normal(rng, (M,))
+    return nodes, fhat, f
+
+
+# ---------------------------------------------------------------- NDFT itself
+
+def test_phase_reduction_is_exact():
+    """(n k) mod 1 against exact rational arithmetic (reading R8)."""
+    rng = np.random.default_rng(1)
+    ks = rng.random(200) - 0.5
+    ns = rng.integers(-2 ** 19, 2 ** 19, 200)
+    for n, k in zip(ns, ks):
+        exact = fractions.Fraction(int(n)) * fractions.Fraction(float(k))
+        exact = exact - round(exact)
+        got = ndft.phase_frac(n, k)
+        assert abs(float(exact) - got) < 2e-16
+
+
+def test_ndft_equispaced_is_a_shifted_dft():
+    """k_j = j/N - 1/2 turns eq. NDFT into a DFT:
+    fhat_j = (-1)^j FFT(f_i (-1)^(i - N/2))_j (library FFT)."""
+    N = 64
+    rng = np.random.default_rng(2)
+    f = workloads.complex_normal(rng, (N,))
+    nodes = (np.arange(N) / N - 0.5)[:, None]
+    i = np.arange(N)
+    ref = (-1.0) ** i * np.fft.fft(f * (-1.0) ** (i - N // 2))
+    got = ndft.ndft(nodes, f, (N,))
+    assert rel_inf(got, ref) < 1e-13
+    # adjoint NDFT on equispaced nodes is N * inverse of the forward
+    y = ndft.adjoint_ndft(nodes, got, (N,))
+    assert rel_inf(y / N, f) < 1e-13
+
+
+def test_ndft_adjointness():
+    nodes, fhat, f = _rand(3, 40, (6, 8))
+    lhs = np.vdot(f, ndft.ndft(nodes, fhat, (6, 8)))
+    rhs = np.vdot(ndft.adjoint_ndft(nodes, f, (6, 8)), fhat)
+    assert abs(lhs - rhs) / abs(lhs) < 1e-13
+
+
+# ------------------------------------------------------- NFFT vs brute force
+
+def test_config1_forward_and_adjoint_match_ndft():
+    """BASELINE configs[0]: 1D N=256, M=256, sigma=2, m=4, seed 0, against
+    the full NDFT. KB at sigma=2, m=4 gives ~5e-8 (error falls ~85x per m)."""
+    w = workloads.make("cfg1_1d_256", seed=0)
+    nodes, fhat, f = w["nodes"], w["fhat"][0], w["f"][0]
+    ref_f = ndft.ndft(nodes, fhat, (256,))
+    ref_y = ndft.adjoint_ndft(nodes, f, (256,))
+    err_f = rel_l2(nfft.forward(nodes, fhat, (256,), 4, 2.0), ref_f)
+    err_y = rel_l2(nfft.adjoint(nodes, f, (256,), 4, 2.0), ref_y)
+    assert 1e-9 < err_f < 2e-7
+    assert 1e-9 < err_y < 2e-7
+    # at m = 8 the KB window reaches fp64 saturation
+    assert rel_l2(nfft.forward(nodes, fhat, (256,), 8, 2.0), ref_f) < 1e-13
+    assert rel_l2(nfft.adjoint(nodes, f, (256,), 8, 2.0), ref_y) < 1e-13
+
+
+@pytest.mark.parametrize("N,M", [((512,), 512), ((32, 32), 1024), ((8, 12, 10), 900)])
+def test_error_decays_exponentially_in_m(N, M):
+    """PAPER.md:714 / 319: the error decreases exponentially with m. For KB at
+    sigma=2 the per-m factor is ~e^{-2 pi sqrt(1-1/sigma)} = 1/85; gate 1/20."""
+    nodes, fhat, f = _rand(4, M, N)
+    ref_f = ndft.ndft(nodes, fhat, N)
+    ref_y = ndft.adjoint_ndft(nodes, f, N)
+    ef, ey = [], []
+    for m in range(2, 7):
+        ef.append(rel_l2(nfft.forward(nodes, fhat, N, m, 2.0), ref_f))
+        ey.append(rel_l2(nfft.adjoint(nodes, f, N, m, 2.0), ref_y))
+    for e in (ef, ey):
+        for a, b in zip(e[:-1], e[1:]):
+            assert b / a < 1 / 20, e
+
+
+def test_error_decay_sigma_125():
+    """sigma = 1.25: slower decay (~e^{-2 pi sqrt(0.2)} = 1/17); gate 1/8."""
+    N, M = (40, 40), 1600
+    nodes, fhat, _ = _rand(5, M, N)
+    ref = ndft.ndft(nodes, fhat, N)
+    e = [rel_l2(nfft.forward(nodes, fhat, N, m, 1.25), ref) for m in range(2, 7)]
+    for a, b in zip(e[:-1], e[1:]):
+        assert b / a < 1 / 8, e
+    # sigma = 1.25 is less accurate than sigma = 2 at the same m
+    assert e[2] > rel_l2(nfft.forward(nodes, fhat, N, 4, 2.0), ref)
+
+
+@pytest.mark.parametrize("N,M", [((64,), 50), ((12, 16), 100), ((8, 8, 10), 77)])
+def test_adjoint_inner_product_identity(N, M):
+    """A ~ B F D and A^H ~ D^T F^H B^T share every factor,
+    so <A fhat, f> = <fhat, A^H f> holds to round-off."""
+    nodes, fhat, f = _rand(6, M, N)
+    for m in (2, 4):
+        Af = nfft.forward(nodes, fhat, N, m, 2.0)
+        AHf = nfft.adjoint(nodes, f, N, m, 2.0)
+        lhs = np.vdot(f, Af)
+        rhs = np.vdot(AHf, fhat)
+        scale = np.linalg.norm(Af) * np.linalg.norm(f)
+        assert abs(lhs - rhs) / scale < 1e-14
+
+
+def test_linearity():
+    N = (16, 16)
+    nodes, f1, _ = _rand(7, 200, N)
+    _, f2, _ = _rand(8, 200, N)
+    a, b = 0.3 - 1.2j, 2.5 + 0.1j
+    lhs = nfft.forward(nodes, a * f1 + b * f2, N, 4, 2.0)
+    rhs = a * nfft.forward(nodes, f1, N, 4, 2.0) + b * nfft.forward(nodes, f2, N, 4, 2.0)
+    assert rel_l2(lhs, rhs) < 1e-14
+
+
+def test_delta_input_gives_ones_on_grid_nodes():
+    """f = delta at n = 0 gives fhat_j = 1 (eq. NDFT). Equispaced nodes are
+    on-grid (t integer) and exercise the floor tie-break (reading R5)."""
+    N = 32
+    nodes = (np.arange(N) / N - 0.5)[:, None]
+    fh = np.zeros(N, complex)
+    fh[N // 2] = 1.0
+    got = nfft.forward(nodes, fh, (N,), 8, 2.0)
+    assert np.max(np.abs(got - 1.0)) < 1e-13
+
+
+def test_single_node_adjoint_gives_ones():
+    """One node at k = 0 with value 1: y_n = e^0 = 1 (eq. NDFTH)."""
+    N = (16, 12)
+    y = nfft.adjoint(np.zeros((1, 2)), np.array([1.0 + 0j]), N, 8, 2.0)
+    assert np.max(np.abs(y - 1.0)) < 1e-13
+
+
+def test_periodicity_of_nodes():
+    """k and k - 1 are the same point of the torus."""
+    N = (24, 20)
+    nodes, fhat, f = _rand(9, 150, N)
+    nodes = np.abs(nodes)
+    shifted = nodes - 1.0
+    a = nfft.forward(nodes, fhat, N, 4, 2.0)
+    b = nfft.forward(shifted, fhat, N, 4, 2.0)
+    assert rel_l2(b, a) < 1e-13
+    assert rel_l2(nfft.adjoint(shifted, f, N, 4, 2.0), nfft.adjoint(nodes, f, N, 4, 2.0)) < 1e-13
+
+
+def test_deconvolution_padding_is_exactly_zero():
+    N = (6, 10)
+    geom = nfft.geometry(N, 2.0, 2)
+    rng = np.random.default_rng(10)
+    g = nfft.deconvolve_pad(workloads.complex_normal(rng, N), geom)
+    mask = np.zeros(geom["Ntilde"], bool)
+    for i in range(-3, 3):
+        for j in range(-5, 5):
+            mask[i % 12, j % 20] = True
+    assert np.all(g[~mask] == 0)
+    assert np.all(g[mask] != 0)
+
+
+def test_fft_conventions():
+    """FFT^H FFT = |I_Ntilde| id; an impulse at l = 0 transforms to all ones."""
+    rng = np.random.default_rng(11)
+    g = workloads.complex_normal(rng, (8, 6))
+    assert rel_inf(nfft.fft_adjoint(nfft.fft_forward(g)), 48 * g) < 1e-14
+    d = np.zeros((8, 6), complex)
+    d[0, 0] = 1
+    assert np.allclose(nfft.fft_forward(d), 1.0)
+
+
+def test_footprint_golden_examples():
+    g = GOLDEN["footprint"]
+    beta = [0.0]
+    l0, W = nfft.local_taps(np.array([g["k"]]), g["Ntilde"], g["m"], 1.0)
+    assert list(range(l0[0], l0[0] + 2 * g["m"])) == g["cells"]
+    g = GOLDEN["footprint_wrap"]
+    l0, W = nfft.local_taps(np.array([g["k"]]), g["Ntilde"], g["m"], 1.0)
+    cells = [(l0[0] + e) % g["Ntilde"] for e in range(2 * g["m"])]
+    assert cells == g["cells_storage"]
+    del beta
+
+
+def test_geometry_validation():
+    assert nfft.geometry((256, 100), 1.25, 4)["Ntilde"] == (320, 126)
+    for bad in [((7,), 2.0, 2), ((8,), 1.0, 2), ((8,), 2.0, 8)]:
+        with pytest.raises(ValueError):
+            nfft.geometry(*bad)
+
+
+@pytest.mark.slow
+def test_full_size_1d_row_sampled_against_ndft():
+    """BASELINE configs[1] (1D N=2^18), m=8, row-sampled exact NDFT: the
+    oracle reaches the fp64 saturation level at full size."""
+    w = workloads.make("cfg2_1d_2e18", seed=0, m=8)
+    rows = np.random.default_rng(12).choice(w["M"], 12, replace=False)
+    ref = ndft.ndft_rows(w["nodes"], w["fhat"][0], w["N"], rows)
+    got = nfft.forward(w["nodes"], w["fhat"][0], w["N"], 8, 2.0, rows=rows)
+    assert rel_l2(got, ref) < 1e-13
