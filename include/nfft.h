@@ -1,0 +1,155 @@
+/*
+ * nfft.h — C ABI of the B200-native NFFT hot path (arXiv:2208.00049, NFFT.jl).
+ *
+ * The library computes the two transforms of the paper with the three steps
+ * of Alg. 1 / Alg. 2: resampling correction (deconvolution
+ * fused with zero-pad / crop), an oversampled FFT (cuFFT, timed separately),
+ * and the Kaiser–Bessel window resampling (hand-written sm_100a kernels).
+ *
+ *   direct  (type-2)  fhat -> f :  f_j  ~ sum_{n in I_N} fhat_n e^{-2 pi i n.k_j}
+ *   adjoint (type-1)  f -> fhat :  y_n  ~ sum_j f_j e^{+2 pi i n.k_j}
+ *
+ * (BASELINE.json's letters: the N-grid array is "fhat", node values are "f";
+ *  the paper uses the opposite letters. Signs are the same.)
+ *
+ * Conventions:
+ *  - nodes: C-contiguous (M, D) reals (float for NFFT_COMPLEX64, double for
+ *    NFFT_COMPLEX128), coordinate d fastest. Nominally in [-1/2, 1/2)^D
+ *    (PAPER.md:90); any finite value is folded periodically.
+ *  - N-grid arrays: C-contiguous (B, N_0, ..., N_{D-1}) interleaved complex
+ *    (re, im) of the plan precision; storage index i_d <-> n_d = i_d - N_d/2,
+ *    n_d in [-N_d/2, N_d/2). Node coordinate d pairs with
+ *    grid axis d; the last axis is contiguous.
+ *  - node-value arrays: (B, M) interleaved complex, caller's node order.
+ *  - Pointers to data may be device pointers or host pointers (pageable or
+ *    pinned); host data is staged through plan-owned device buffers on the
+ *    plan stream (detected with cudaPointerGetAttributes).
+ *  - All work is enqueued on the plan's stream; calls return after enqueue
+ *    except where noted (host outputs are complete on return).
+ *  - One transform per plan at a time (the plan owns its scratch).
+ *
+ * Errors: every function returns nfft_status; arguments are validated before
+ * anything is enqueued and a failed call leaves the plan unchanged. No C++
+ * exception crosses this boundary. Asynchronous CUDA faults surface as
+ * NFFT_ERROR_CUDA on a later call.
+ */
+#ifndef NFFT_B200_H
+#define NFFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nfft_plan_s* nfft_plan; /* opaque; created and owned by the library */
+
+/* Window pair: Kaiser–Bessel, beta = pi m (2 - 1/sigma). */
+typedef enum { NFFT_WINDOW_KAISER_BESSEL = 0 } nfft_window;
+
+/* Complex{T} data with real-T nodes. */
+typedef enum { NFFT_COMPLEX64 = 0, NFFT_COMPLEX128 = 1 } nfft_precision;
+
+typedef enum {
+  NFFT_SUCCESS = 0,
+  NFFT_ERROR_INVALID_VALUE = 1,   /* null pointer, D not in 1..3, M < 1, m < 1, B < 1, unknown enum */
+  NFFT_ERROR_BAD_GEOMETRY = 2,    /* odd or < 2 N_d, sigma <= 1, 2m >= Ntilde_d */
+  NFFT_ERROR_NONFINITE_NODE = 3,  /* a node coordinate is NaN/Inf (reported by nfft_precompute) */
+  NFFT_ERROR_BAD_TILE = 4,        /* tile_d < 0, tile_d > Ntilde_d, or tile+halo exceeds shared memory */
+  NFFT_ERROR_NOT_PRECOMPUTED = 5, /* forward/adjoint before nfft_precompute */
+  NFFT_ERROR_OUT_OF_MEMORY = 6,
+  NFFT_ERROR_CUDA = 7,
+  NFFT_ERROR_CUFFT = 8,
+  NFFT_ERROR_UNSUPPORTED = 9      /* D > 3, m > 8, or sizes beyond int32 indexing */
+} nfft_status;
+
+/* Resampling kernels. */
+typedef enum {
+  NFFT_METHOD_AUTO = 0,   /* tiled when the tile+halo fits shared memory */
+  NFFT_METHOD_TILED = 1,  /* Alg. 3/4: grid tile + m-halo staged in shared memory */
+  NFFT_METHOD_DIRECT = 2  /* unblocked resampling straight from L2/HBM */
+} nfft_method;
+
+typedef struct {
+  int64_t batch;          /* B >= 1 transforms sharing the nodes (default 1) */
+  int64_t tile[3];        /* block size Q_d in grid cells; 0 = default */
+  void* stream;           /* cudaStream_t for all work; NULL = legacy default stream */
+  int device;             /* CUDA device ordinal; -1 = current device */
+  int method;             /* nfft_method */
+  int64_t max_subproblem; /* max nodes per CTA (splits dense tiles); 0 = default */
+  int64_t node_begin;     /* shard [node_begin, node_end) of the TILE-SORTED node order that */
+  int64_t node_end;       /*   forward/adjoint process; node_end = 0 means M (all nodes) */
+  int timing;             /* 1: record CUDA events around every stage (nfft_get_stage_times) */
+  int check_nodes;        /* 1 (default): nfft_precompute synchronises once and reports
+                             NFFT_ERROR_NONFINITE_NODE; 0: fully asynchronous, no check
+                             (non-finite nodes then give unspecified values, never a fault) */
+} nfft_options;
+
+/* Fills *opt with the defaults above. */
+nfft_status nfft_default_options(nfft_options* opt);
+
+/*
+ * Creates a plan: validates the geometry,
+ * computes Ntilde_d = 2 ceil(sigma N_d / 2), allocates the oversampled grid
+ * (B * prod Ntilde complex), the cuFFT plan and node buffers, and COPIES the
+ * M*D node coordinates (host or device pointer) into plan storage; the
+ * caller may free `nodes` on return. N points to D int64 sizes.
+ */
+nfft_status nfft_plan_create(nfft_plan* out, int D, const int64_t* N, int64_t M, const void* nodes,
+                             double sigma, int m, nfft_window window, nfft_precision precision);
+nfft_status nfft_plan_create_ex(nfft_plan* out, int D, const int64_t* N, int64_t M, const void* nodes,
+                                double sigma, int m, nfft_window window, nfft_precision precision,
+                                const nfft_options* opt);
+
+/* Replaces the node coordinates (same M); the plan must be re-precomputed. */
+nfft_status nfft_set_nodes(nfft_plan p, const void* nodes);
+
+/*
+ * Precompute, all on the device:
+ * bins every node into its tile (fp64 t = Ntilde k, a = floor t), stable
+ * radix sort by tile id -> perm and tile offsets, sorted coordinates,
+ * subproblem list, beta^tensor correction vectors and the piecewise
+ * polynomial window table. With options.check_nodes = 1 (default) it
+ * synchronises the stream once to report NFFT_ERROR_NONFINITE_NODE.
+ */
+nfft_status nfft_precompute(nfft_plan p);
+
+/* Direct NFFT, Alg. 1: fhat_grid (B, N...) -> f_nodes (B, M).
+ * Only nodes of the plan's shard are written. */
+nfft_status nfft_forward(nfft_plan p, const void* fhat_grid, void* f_nodes);
+
+/* Adjoint NFFT, Alg. 2: f_nodes (B, M) -> fhat_grid (B, N...).
+ * Only nodes of the plan's shard contribute (linearity: shards sum). */
+nfft_status nfft_adjoint(nfft_plan p, const void* f_nodes, void* fhat_grid);
+
+nfft_status nfft_plan_destroy(nfft_plan p);
+const char* nfft_status_string(nfft_status s);
+
+/* ---- introspection for tests and bench ---- */
+
+/* Ntilde (D entries), tile Q (D), tiles per dim P (D); n_tiles = prod P. Any pointer may be NULL. */
+nfft_status nfft_plan_info(nfft_plan p, int64_t* Ntilde, int64_t* tile, int64_t* tiles_per_dim, int64_t* n_tiles);
+
+/* Copies perm (M int32) and tile offsets (n_tiles+1 int32) to host memory;
+ * synchronises the plan stream. Either pointer may be NULL. */
+nfft_status nfft_get_binning(nfft_plan p, int32_t* perm_host, int32_t* tile_offsets_host);
+
+/* Copies the window tables to host: beta^tensor (sum_d N_d doubles, dim 0
+ * first) and the polynomial coefficients (D * 2m * (deg+1) doubles,
+ * [d][tap][z]); *deg receives the polynomial degree. Synchronises. */
+nfft_status nfft_get_window_tables(nfft_plan p, double* beta_tensor, double* poly, int* deg);
+
+/* Milliseconds of the most recent forward/adjoint stages (timing = 1):
+ * ms[0] deconv/pad or crop/deconv, ms[1] cuFFT, ms[2] resampling kernel,
+ * ms[3] grid zeroing (adjoint), ms[4] precompute. Synchronises. */
+nfft_status nfft_get_stage_times(nfft_plan p, int which /* 0 forward, 1 adjoint */, float* ms5);
+
+/* Number of this library's own kernel launches since plan creation
+ * (cuFFT's kernels are not counted). */
+nfft_status nfft_get_launch_count(nfft_plan p, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NFFT_B200_H */

@@ -1,0 +1,290 @@
+"""B200-native NFFT hot path (arXiv:2208.00049, NFFT.jl) — Python binding.
+
+A thin ctypes layer over the C ABI in include/nfft.h (libnfft_b200.so, built
+in-tree by `__graft_entry__.build()` / `python -m paper_2208_00049_b200.build`).
+It only marshals arguments: every step of the transform runs in the library's
+CUDA kernels (and cuFFT for the oversampled FFT). PyTorch is used for device
+memory and streams. There is no CPU fallback: if the shared library is
+missing, importing `lib()` raises.
+
+    plan = NfftPlan(nodes, N=(512, 512), m=4, sigma=2.0)
+    plan.precompute()
+    f = plan.forward(fhat)      # direct NFFT, Alg. 1
+    y = plan.adjoint(f)         # adjoint NFFT, Alg. 2
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnfft_b200.so")
+
+# Every symbol include/nfft.h declares (checked by tests/test_abi.py).
+NFFT_SYMBOLS = (
+    "nfft_default_options", "nfft_plan_create", "nfft_plan_create_ex", "nfft_set_nodes",
+    "nfft_precompute", "nfft_forward", "nfft_adjoint", "nfft_plan_destroy", "nfft_status_string",
+    "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
+    "nfft_get_launch_count",
+)
+
+STATUS = {
+    0: "NFFT_SUCCESS", 1: "NFFT_ERROR_INVALID_VALUE", 2: "NFFT_ERROR_BAD_GEOMETRY",
+    3: "NFFT_ERROR_NONFINITE_NODE", 4: "NFFT_ERROR_BAD_TILE", 5: "NFFT_ERROR_NOT_PRECOMPUTED",
+    6: "NFFT_ERROR_OUT_OF_MEMORY", 7: "NFFT_ERROR_CUDA", 8: "NFFT_ERROR_CUFFT", 9: "NFFT_ERROR_UNSUPPORTED",
+}
+METHODS = {"auto": 0, "tiled": 1, "direct": 2}
+PRECISIONS = {"c64": 0, "c128": 1}
+
+
+class NfftError(RuntimeError):
+    def __init__(self, status, what):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{what}: {self.name} ({_lib.nfft_status_string(status).decode()})")
+
+
+class Options(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int64), ("tile", ctypes.c_int64 * 3), ("stream", ctypes.c_void_p),
+        ("device", ctypes.c_int), ("method", ctypes.c_int), ("max_subproblem", ctypes.c_int64),
+        ("node_begin", ctypes.c_int64), ("node_end", ctypes.c_int64), ("timing", ctypes.c_int),
+        ("check_nodes", ctypes.c_int),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libnfft_b200.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2208_00049_b200.build` "
+                          "(or __graft_entry__.build()). There is no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, c_int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
+    P = ctypes.POINTER
+    sigs = {
+        "nfft_default_options": [P(Options)],
+        "nfft_plan_create": [P(vp), c_int, P(i64), i64, vp, ctypes.c_double, c_int, c_int, c_int],
+        "nfft_plan_create_ex": [P(vp), c_int, P(i64), i64, vp, ctypes.c_double, c_int, c_int, c_int, P(Options)],
+        "nfft_set_nodes": [vp, vp],
+        "nfft_precompute": [vp],
+        "nfft_forward": [vp, vp, vp],
+        "nfft_adjoint": [vp, vp, vp],
+        "nfft_plan_destroy": [vp],
+        "nfft_plan_info": [vp, P(i64), P(i64), P(i64), P(i64)],
+        "nfft_get_binning": [vp, P(i32), P(i32)],
+        "nfft_get_window_tables": [vp, P(ctypes.c_double), P(ctypes.c_double), P(c_int)],
+        "nfft_get_stage_times": [vp, c_int, P(ctypes.c_float)],
+        "nfft_get_launch_count": [vp, P(i64)],
+    }
+    for name, args in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = c_int
+    L.nfft_status_string.argtypes = [c_int]
+    L.nfft_status_string.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(status, what):
+    if status != 0:
+        raise NfftError(status, what)
+
+
+def _ptr(x):
+    """Device pointer of a torch tensor or host pointer of a numpy array."""
+    if isinstance(x, np.ndarray):
+        return ctypes.c_void_p(x.ctypes.data)
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class NfftPlan:
+    """NFFT plan over fixed nodes.
+
+    nodes: (M, D) float64 (c128) or float32 (c64), torch (any device) or numpy.
+    N: grid size per dimension (even). Outputs follow the inputs: torch CUDA in
+    -> torch CUDA out; numpy in -> numpy out (host staging inside the library).
+    node_range: (begin, end) shard of the TILE-SORTED node order processed by
+    forward/adjoint (multi-GPU sharding).
+    """
+
+    def __init__(self, nodes, N, m=4, sigma=2.0, precision="c128", batch=1, tile=None, stream=None,
+                 device=None, method="auto", max_subproblem=0, node_range=None, timing=False,
+                 check_nodes=True):
+        L = lib()
+        self.N = tuple(int(n) for n in N)
+        self.D = len(self.N)
+        self.m = int(m)
+        self.sigma = float(sigma)
+        self.precision = precision
+        self.batch = int(batch)
+        self.rdtype = np.float64 if precision == "c128" else np.float32
+        self.cdtype = np.complex128 if precision == "c128" else np.complex64
+        torch = _torch()
+        self.tdtype_c = torch.complex128 if precision == "c128" else torch.complex64
+        self.tdtype_r = torch.float64 if precision == "c128" else torch.float32
+        if device is None:
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        self.device = int(device)
+        if stream is None and torch.cuda.is_available():
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.stream = stream
+        nodes = self._nodes_arg(nodes)
+        self.M = int(nodes.shape[0])
+        opt = Options()
+        L.nfft_default_options(ctypes.byref(opt))
+        opt.batch = self.batch
+        for d, q in enumerate(tile or ()):
+            opt.tile[d] = int(q)
+        opt.stream = stream
+        opt.device = self.device
+        opt.method = METHODS[method]
+        opt.max_subproblem = int(max_subproblem)
+        if node_range is not None:
+            opt.node_begin, opt.node_end = int(node_range[0]), int(node_range[1])
+        opt.timing = int(bool(timing))
+        opt.check_nodes = int(bool(check_nodes))
+        self.opts = opt
+        Narr = (ctypes.c_int64 * self.D)(*self.N)
+        h = ctypes.c_void_p()
+        _check(L.nfft_plan_create_ex(ctypes.byref(h), self.D, Narr, self.M, _ptr(nodes), self.sigma, self.m, 0,
+                                     PRECISIONS[precision], ctypes.byref(opt)), "nfft_plan_create")
+        self._h = h
+        self._keep = nodes  # keep the source alive until the async copy is done
+        self.precomputed = False
+
+    # -- argument marshalling ------------------------------------------------
+    def _nodes_arg(self, nodes):
+        torch = _torch()
+        if isinstance(nodes, np.ndarray):
+            return np.ascontiguousarray(nodes.reshape(nodes.shape[0], -1), dtype=self.rdtype)
+        t = nodes.reshape(nodes.shape[0], -1)
+        if t.dtype != self.tdtype_r or not t.is_contiguous():
+            t = t.to(self.tdtype_r).contiguous()
+        return t
+
+    def _grid_shape(self):
+        return (self.batch,) + self.N
+
+    def _data_arg(self, x, shape):
+        torch = _torch()
+        if isinstance(x, np.ndarray):
+            x = np.ascontiguousarray(x, dtype=self.cdtype)
+            if x.size != int(np.prod(shape)):
+                raise ValueError(f"expected {shape} elements, got {x.shape}")
+            return x
+        if x.dtype != self.tdtype_c or not x.is_contiguous():
+            x = x.to(self.tdtype_c).contiguous()
+        if x.numel() != int(np.prod(shape)):
+            raise ValueError(f"expected {shape} elements, got {tuple(x.shape)}")
+        return x
+
+    def _empty_like_kind(self, ref, shape):
+        if isinstance(ref, np.ndarray):
+            return np.empty(shape, dtype=self.cdtype)
+        torch = _torch()
+        return torch.empty(shape, dtype=self.tdtype_c, device=ref.device)
+
+    # -- ABI calls -----------------------------------------------------------
+    def set_nodes(self, nodes):
+        nodes = self._nodes_arg(nodes)
+        _check(lib().nfft_set_nodes(self._h, _ptr(nodes)), "nfft_set_nodes")
+        self._keep = nodes
+        self.precomputed = False
+
+    def precompute(self):
+        _check(lib().nfft_precompute(self._h), "nfft_precompute")
+        self.precomputed = True
+        return self
+
+    def forward(self, fhat, out=None):
+        """Direct NFFT: fhat (B, *N) or (*N) -> f (B, M)."""
+        fhat = self._data_arg(fhat, self._grid_shape())
+        if out is None:
+            out = self._empty_like_kind(fhat, (self.batch, self.M))
+        _check(lib().nfft_forward(self._h, _ptr(fhat), _ptr(out)), "nfft_forward")
+        return out
+
+    def adjoint(self, f, out=None):
+        """Adjoint NFFT: f (B, M) or (M,) -> y (B, *N)."""
+        f = self._data_arg(f, (self.batch, self.M))
+        if out is None:
+            out = self._empty_like_kind(f, self._grid_shape())
+        _check(lib().nfft_adjoint(self._h, _ptr(f), _ptr(out)), "nfft_adjoint")
+        return out
+
+    def info(self):
+        nt = (ctypes.c_int64 * 3)()
+        q = (ctypes.c_int64 * 3)()
+        p = (ctypes.c_int64 * 3)()
+        n = ctypes.c_int64()
+        _check(lib().nfft_plan_info(self._h, nt, q, p, ctypes.byref(n)), "nfft_plan_info")
+        return dict(Ntilde=tuple(nt[: self.D]), tile=tuple(q[: self.D]), tiles_per_dim=tuple(p[: self.D]),
+                    n_tiles=n.value)
+
+    def binning(self):
+        n_tiles = self.info()["n_tiles"]
+        perm = np.empty(self.M, np.int32)
+        offs = np.empty(n_tiles + 1, np.int32)
+        _check(lib().nfft_get_binning(self._h, perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                      offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), "nfft_get_binning")
+        return perm, offs
+
+    def window_tables(self):
+        deg = ctypes.c_int()
+        _check(lib().nfft_get_window_tables(self._h, None, None, ctypes.byref(deg)), "nfft_get_window_tables")
+        beta = np.empty(sum(self.N), np.float64)
+        poly = np.empty((self.D, 2 * self.m, deg.value + 1), np.float64)
+        _check(lib().nfft_get_window_tables(self._h, beta.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            poly.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            ctypes.byref(deg)), "nfft_get_window_tables")
+        return beta, poly, deg.value
+
+    def stage_times(self, which):
+        ms = (ctypes.c_float * 5)()
+        _check(lib().nfft_get_stage_times(self._h, 0 if which == "forward" else 1, ms), "nfft_get_stage_times")
+        return dict(deconv=ms[0], fft=ms[1], resample=ms[2], zero=ms[3], precompute=ms[4])
+
+    def launches(self):
+        n = ctypes.c_int64()
+        _check(lib().nfft_get_launch_count(self._h, ctypes.byref(n)), "nfft_get_launch_count")
+        return n.value
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _check(lib().nfft_plan_destroy(self._h), "nfft_plan_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nfft(nodes, fhat, N, m=4, sigma=2.0, precision="c128"):
+    """One-shot direct NFFT."""
+    p = NfftPlan(nodes, N, m=m, sigma=sigma, precision=precision).precompute()
+    out = p.forward(fhat)
+    p.close()
+    return out
+
+
+def nfft_adjoint(nodes, N, f, m=4, sigma=2.0, precision="c128"):
+    """One-shot adjoint NFFT."""
+    p = NfftPlan(nodes, N, m=m, sigma=sigma, precision=precision).precompute()
+    out = p.adjoint(f)
+    p.close()
+    return out

@@ -1,0 +1,116 @@
+// common.cuh — shared types and device helpers of the sm_100a NFFT path.
+// (Product code; shares nothing with oracle/.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nfftb {
+
+constexpr int MAX_D = 3;
+constexpr int MAX_M = 8;    // half-width m; 2m taps per dimension
+constexpr int MAX_Z = 17;   // polynomial coefficients per tap (degree <= 16)
+constexpr int THREADS = 256;
+
+// Window-table degree (DESIGN.md §Window tables): the paper's degree 2m
+// is raised to 14 in fp64 so the table error (~1e-14 of the
+// peak) stays far below the 1e-12 parity bar; fp32 uses max(2m, 8).
+__host__ __device__ constexpr int poly_degree(int m, bool fp64) {
+  return fp64 ? (2 * m > 14 ? 2 * m : 14) : (2 * m > 8 ? 2 * m : 8);
+}
+
+template <typename T> struct cplx;
+template <> struct cplx<double> { using type = double2; };
+template <> struct cplx<float> { using type = float2; };
+
+// Geometry passed by value to every kernel.
+struct Geom {
+  int D;
+  int M;          // number of nodes
+  int B;          // batch
+  int m;          // half-width
+  int Nt[MAX_D];  // oversampled size Ntilde_d
+  int N[MAX_D];   // N_d
+  int Q[MAX_D];   // tile size
+  int P[MAX_D];   // tiles per dimension
+  int L[MAX_D];   // tile region extent Q_d + 2m - 1
+  double Ntd[MAX_D];
+  long long grid_cells;   // prod Ntilde
+  long long ngrid_cells;  // prod N
+  int region_cells;       // prod L
+  int beta_off[MAX_D];    // offset of dim d in the beta^tensor vector
+};
+
+// Piecewise-polynomial window table for taps 0..m-1 of each dimension
+// (taps m..2m-1 are their mirrors, see taps()). Passed as a kernel parameter
+// so every coefficient is a constant-bank operand of the FMA.
+template <typename T> struct WinPoly { T mu[MAX_D][MAX_M][MAX_Z]; };
+
+// Cell of a node along one dimension (reading R5/R10):
+// t = Ntilde * k (one IEEE multiply, never contracted), a = floor(t),
+// frac = t - a (exact), c = (a + Ntilde/2) mod Ntilde in [0, Ntilde).
+__device__ __forceinline__ int node_cell(double k, double Ntd, int Nt, double& frac) {
+  const double t = __dmul_rn(Ntd, k);
+  const double a = floor(t);
+  frac = t - a;
+  const double r = fmod(a, Ntd);  // exact for integer-valued doubles, |r| < Ntilde
+  int c = (int)r + (Nt >> 1);
+  if (c < 0) c += Nt;
+  else if (c >= Nt) c -= Nt;
+  return c;
+}
+
+__device__ __forceinline__ int pos_mod(int a, int n) {
+  int r = a % n;
+  return r < 0 ? r + n : r;
+}
+
+// 2m window taps from the polynomial table at zeta = frac - 1/2.
+// Tap l (cell a-m+1+l) and tap 2m-1-l are mirror images, w_{2m-1-l}(zeta) =
+// w_l(-zeta) (the window is even), so with p_l = E(zeta^2) + zeta O(zeta^2):
+// w_l = E + zeta O, w_{2m-1-l} = E - zeta O.
+template <typename T, int M, int DEG>
+__device__ __forceinline__ void window_taps(T zeta, const T (&mu)[MAX_M][MAX_Z], T (&w)[2 * M]) {
+  const T z2 = zeta * zeta;
+#pragma unroll
+  for (int l = 0; l < M; ++l) {
+    T e = mu[l][DEG];
+#pragma unroll
+    for (int z = DEG - 2; z >= 0; z -= 2) e = fma(e, z2, mu[l][z]);
+    T o = mu[l][DEG - 1];
+#pragma unroll
+    for (int z = DEG - 3; z >= 1; z -= 2) o = fma(o, z2, mu[l][z]);
+    w[l] = fma(zeta, o, e);
+    w[2 * M - 1 - l] = fma(-zeta, o, e);
+  }
+}
+
+// ---- block-wide exclusive scan of one int per thread (blockDim = THREADS) ----
+__device__ __forceinline__ int block_exclusive_scan(int x, int* ws, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) ws[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < nw ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) ws[lane] = t;
+  }
+  __syncthreads();
+  const int prefix = w > 0 ? ws[w - 1] : 0;
+  total = ws[nw - 1];
+  __syncthreads();
+  return prefix + inc - x;
+}
+
+}  // namespace nfftb

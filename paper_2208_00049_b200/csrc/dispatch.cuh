@@ -1,0 +1,59 @@
+// dispatch.cuh — kernel-pointer sets per (precision, D, m). The template
+// instantiations live in inst_d{1,2,3}.cu so they compile in parallel.
+#pragma once
+
+#include "common.cuh"
+
+namespace nfftb {
+
+template <typename T>
+struct KernelSet {
+  using C = typename cplx<T>::type;
+  void (*interp_tiled)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
+  void (*spread_tiled)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
+  void (*interp_direct)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, C*);
+  void (*spread_direct)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, C*);
+};
+
+template <typename T> KernelSet<T> kernels_d1(int m);
+template <typename T> KernelSet<T> kernels_d2(int m);
+template <typename T> KernelSet<T> kernels_d3(int m);
+
+template <typename T>
+inline KernelSet<T> kernels_for(int D, int m) {
+  if (D == 1) return kernels_d1<T>(m);
+  if (D == 2) return kernels_d2<T>(m);
+  return kernels_d3<T>(m);
+}
+
+}  // namespace nfftb
+
+#ifdef NFFTB_INSTANTIATE_D
+#include "resample.cuh"
+namespace nfftb {
+template <typename T, int D, int M>
+KernelSet<T> make_set() {
+  constexpr int DEG = poly_degree(M, sizeof(T) == 8);
+  return {interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>, interp_direct_kernel<T, D, M, DEG>,
+          spread_direct_kernel<T, D, M, DEG>};
+}
+template <typename T, int D>
+KernelSet<T> make_set_m(int m) {
+  switch (m) {
+    case 1: return make_set<T, D, 1>();
+    case 2: return make_set<T, D, 2>();
+    case 3: return make_set<T, D, 3>();
+    case 4: return make_set<T, D, 4>();
+    case 5: return make_set<T, D, 5>();
+    case 6: return make_set<T, D, 6>();
+    case 7: return make_set<T, D, 7>();
+    default: return make_set<T, D, 8>();
+  }
+}
+}  // namespace nfftb
+#define NFFTB_DEFINE_D(FN, D)                                          \
+  namespace nfftb {                                                    \
+  template <> KernelSet<double> FN<double>(int m) { return make_set_m<double, D>(m); } \
+  template <> KernelSet<float> FN<float>(int m) { return make_set_m<float, D>(m); }    \
+  }
+#endif

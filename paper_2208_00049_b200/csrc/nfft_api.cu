@@ -1,0 +1,756 @@
+// nfft_api.cu — plan object, orchestration and the C ABI of include/nfft.h.
+//
+// Host side of the B200 NFFT: validates the geometry,
+// owns every device buffer (the paper's plan as preallocated state,
+// PAPER.md:374-382), builds the window tables and cuFFT plan once, and
+// enqueues the kernels of precompute.cuh / grid.cuh / resample.cuh on the
+// plan stream. Nothing here computes on the host except geometry and launch
+// configuration.
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/nfft.h"
+#include "common.cuh"
+#include "dispatch.cuh"
+#include "grid.cuh"
+#include "precompute.cuh"
+
+using namespace nfftb;
+
+struct nfft_plan_s;
+template <typename T> const KernelSet<T>& kernels_of(const nfft_plan_s* p);
+template <typename T> const WinPoly<T>& poly_of(const nfft_plan_s* p);
+
+struct nfft_plan_s {
+  int D = 0;
+  int64_t N[3] = {1, 1, 1}, Nt[3] = {1, 1, 1}, Q[3] = {1, 1, 1}, P[3] = {1, 1, 1};
+  int64_t M = 0, B = 1;
+  int m = 0;
+  double sigma = 0;
+  double beta[3] = {0, 0, 0};
+  nfft_precision prec = NFFT_COMPLEX128;
+  nfft_options opt{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  bool tiled = true;
+  int S = 256;            // max nodes per subproblem
+  int node_begin = 0, node_end = 0;
+  int64_t n_tiles = 1;
+  int deg = 14;
+  int nbits = 0;
+  int sort_blocks = 1;
+  int max_subs = 1;
+  int grid_tiled = 1;     // CTAs for the tiled kernels
+  int grid_direct = 1;
+  size_t region_bytes = 0;
+  Geom geom{};
+  WinPoly<double> wp64{};
+  WinPoly<float> wp32{};
+  KernelSet<double> k64{};
+  KernelSet<float> k32{};
+  // device buffers
+  void* d_nodes = nullptr;   // M*D reals (plan precision)
+  void* d_ks = nullptr;      // D*M sorted reals
+  int* d_keys_a = nullptr;
+  int* d_vals_a = nullptr;
+  int* d_keys_b = nullptr;
+  int* d_vals_b = nullptr;
+  int* d_perm = nullptr;     // points at the sorted vals buffer
+  int* d_offsets = nullptr;  // n_tiles + 1
+  int* d_hist = nullptr;     // 256 * sort_blocks
+  int* d_scan_tmp = nullptr;
+  int* d_subbase = nullptr;  // n_tiles + 1 (last = number of subproblems)
+  int4* d_subs = nullptr;
+  int* d_err = nullptr;
+  void* d_grid = nullptr;    // B * prod Nt complex
+  double* d_beta64 = nullptr;
+  void* d_betaT = nullptr;
+  double* d_poly = nullptr;  // D*2m*MAX_Z
+  void* d_stage_grid = nullptr;   // B * prod N complex (host-pointer staging)
+  void* d_stage_nodes = nullptr;  // B * M complex
+  cufftHandle fft = 0;
+  bool fft_ok = false;
+  bool precomputed = false;
+  cudaEvent_t ev[3][6] = {};
+  bool events = false;
+  int64_t launches = 0;
+  size_t csize() const { return prec == NFFT_COMPLEX128 ? 16 : 8; }
+  size_t rsize() const { return prec == NFFT_COMPLEX128 ? 8 : 4; }
+};
+
+template <> const KernelSet<double>& kernels_of<double>(const nfft_plan_s* p) { return p->k64; }
+template <> const KernelSet<float>& kernels_of<float>(const nfft_plan_s* p) { return p->k32; }
+template <> const WinPoly<double>& poly_of<double>(const nfft_plan_s* p) { return p->wp64; }
+template <> const WinPoly<float>& poly_of<float>(const nfft_plan_s* p) { return p->wp32; }
+
+namespace {
+
+#define CK(call)                                    \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) {                        \
+      last_cuda_error = e_;                         \
+      return NFFT_ERROR_CUDA;                       \
+    }                                               \
+  } while (0)
+
+#define CKL()                                       \
+  do {                                              \
+    cudaError_t e_ = cudaGetLastError();            \
+    if (e_ != cudaSuccess) {                        \
+      last_cuda_error = e_;                         \
+      return NFFT_ERROR_CUDA;                       \
+    }                                               \
+  } while (0)
+
+thread_local cudaError_t last_cuda_error = cudaSuccess;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_pointer(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void free_all(nfft_plan p) {
+  void* bufs[] = {p->d_nodes, p->d_ks, p->d_keys_a, p->d_vals_a, p->d_keys_b, p->d_vals_b, p->d_offsets,
+                  p->d_hist, p->d_scan_tmp, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_beta64,
+                  p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (p->fft_ok) cufftDestroy(p->fft);
+  if (p->events)
+    for (auto& row : p->ev)
+      for (auto& e : row)
+        if (e) cudaEventDestroy(e);
+}
+
+nfft_status scan_exclusive(nfft_plan p, int* d, int n, int* tmp) {
+  const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  scan_tile_kernel<<<nb, THREADS, 0, p->stream>>>(d, d, n, nb > 1 ? tmp : nullptr);
+  ++p->launches;
+  CKL();
+  if (nb > 1) {
+    nfft_status s = scan_exclusive(p, tmp, nb, tmp + nb);
+    if (s != NFFT_SUCCESS) return s;
+    scan_add_kernel<<<nb, THREADS, 0, p->stream>>>(d, n, tmp);
+    ++p->launches;
+    CKL();
+  }
+  return NFFT_SUCCESS;
+}
+
+size_t scan_tmp_ints(int64_t n) {
+  size_t total = 0;
+  int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  while (nb > 1) {
+    total += nb;
+    nb = (nb + SCAN_TILE - 1) / SCAN_TILE;
+  }
+  return total + 64;
+}
+
+inline void rec(nfft_plan p, int which, int slot) {
+  if (p->events) cudaEventRecord(p->ev[which][slot], p->stream);
+}
+
+template <typename T>
+nfft_status build_window_tables(nfft_plan p) {
+  const int n = (int)(p->N[0] + (p->D > 1 ? p->N[1] : 0) + (p->D > 2 ? p->N[2] : 0));
+  beta_tensor_kernel<T><<<(n + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
+      p->geom, p->beta[0], p->beta[1], p->beta[2], p->d_beta64, (T*)p->d_betaT);
+  ++p->launches;
+  CKL();
+  const int nfit = p->D * 2 * p->m;
+  poly_fit_kernel<<<(nfit + 63) / 64, 64, 0, p->stream>>>(p->D, p->m, p->deg + 1, p->beta[0], p->beta[1], p->beta[2],
+                                                          p->d_poly);
+  ++p->launches;
+  CKL();
+  const size_t cnt = (size_t)nfit * MAX_Z;
+  double* host = new (std::nothrow) double[cnt];
+  if (!host) return NFFT_ERROR_OUT_OF_MEMORY;
+  cudaError_t e = cudaMemcpyAsync(host, p->d_poly, cnt * sizeof(double), cudaMemcpyDeviceToHost, p->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  if (e != cudaSuccess) {
+    delete[] host;
+    last_cuda_error = e;
+    return NFFT_ERROR_CUDA;
+  }
+  memset(&p->wp64, 0, sizeof(p->wp64));
+  memset(&p->wp32, 0, sizeof(p->wp32));
+  for (int d = 0; d < p->D; ++d)
+    for (int l = 0; l < p->m; ++l)
+      for (int z = 0; z < MAX_Z; ++z) {
+        const double v = host[((size_t)d * 2 * p->m + l) * MAX_Z + z];
+        p->wp64.mu[d][l][z] = v;
+        p->wp32.mu[d][l][z] = (float)v;
+      }
+  delete[] host;
+  return NFFT_SUCCESS;
+}
+
+template <typename T>
+nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
+  if (p->tiled) {
+    const void* fns[2] = {(const void*)ks.interp_tiled, (const void*)ks.spread_tiled};
+    int occ_min = 1 << 30;
+    for (const void* fn : fns) {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->region_bytes));
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, p->region_bytes));
+      if (occ < 1) return NFFT_ERROR_BAD_TILE;
+      occ_min = std::min(occ_min, occ);
+    }
+    p->grid_tiled = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ_min * p->sm_count));
+  }
+  p->grid_direct = p->sm_count * 8;
+  return NFFT_SUCCESS;
+}
+
+template <typename R>
+nfft_status precompute_impl(nfft_plan p) {
+  const int M = (int)p->M;
+  const int nb_bin = (M + THREADS - 1) / THREADS;
+  CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->stream));
+  rec(p, 2, 0);
+  bin_nodes_kernel<R><<<nb_bin, THREADS, 0, p->stream>>>((const R*)p->d_nodes, p->geom, p->d_keys_a, p->d_vals_a,
+                                                         p->d_err);
+  ++p->launches;
+  CKL();
+  int* ka = p->d_keys_a;
+  int* va = p->d_vals_a;
+  int* kb = p->d_keys_b;
+  int* vb = p->d_vals_b;
+  for (int shift = 0; shift < p->nbits; shift += 8) {
+    const int bits = std::min(8, p->nbits - shift);
+    radix_hist_kernel<<<p->sort_blocks, THREADS, 0, p->stream>>>(ka, M, shift, p->sort_blocks, p->d_hist);
+    ++p->launches;
+    CKL();
+    nfft_status s = scan_exclusive(p, p->d_hist, 256 * p->sort_blocks, p->d_scan_tmp);
+    if (s != NFFT_SUCCESS) return s;
+    radix_scatter_kernel<<<p->sort_blocks, THREADS, 0, p->stream>>>(ka, va, kb, vb, M, shift, bits, p->sort_blocks,
+                                                                      p->d_hist);
+    ++p->launches;
+    CKL();
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  p->d_perm = va;
+  const int nt = (int)p->n_tiles;
+  tile_offsets_kernel<<<(M + 1 + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(ka, M, nt, p->d_offsets);
+  ++p->launches;
+  CKL();
+  gather_sorted_kernel<R><<<nb_bin, THREADS, 0, p->stream>>>((const R*)p->d_nodes, p->d_perm, p->geom, (R*)p->d_ks);
+  ++p->launches;
+  CKL();
+  if (p->tiled) {
+    count_subproblems_kernel<<<(nt + 1 + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
+        p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase);
+    ++p->launches;
+    CKL();
+    nfft_status s = scan_exclusive(p, p->d_subbase, nt + 1, p->d_scan_tmp);
+    if (s != NFFT_SUCCESS) return s;
+    write_subproblems_kernel<<<(nt + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
+        p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase, p->d_subs);
+    ++p->launches;
+    CKL();
+  }
+  rec(p, 2, 1);
+  return NFFT_SUCCESS;
+}
+
+template <typename T>
+nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
+  using C = typename cplx<T>::type;
+  const KernelSet<T>& ks = kernels_of<T>(p);
+  const WinPoly<T>& wp = poly_of<T>(p);
+  const size_t grid_bytes_in = (size_t)p->B * p->geom.ngrid_cells * sizeof(C);
+  const size_t node_bytes = (size_t)p->B * p->M * sizeof(C);
+  const C* fhat = (const C*)fhat_in;
+  C* f = (C*)f_out;
+  const bool host_in = !is_device_pointer(fhat_in);
+  const bool host_out = !is_device_pointer(f_out);
+  if (host_in) {
+    if (!p->d_stage_grid) CK(cudaMalloc(&p->d_stage_grid, grid_bytes_in));
+    CK(cudaMemcpyAsync(p->d_stage_grid, fhat_in, grid_bytes_in, cudaMemcpyHostToDevice, p->stream));
+    fhat = (const C*)p->d_stage_grid;
+  }
+  if (host_out) {
+    if (!p->d_stage_nodes) CK(cudaMalloc(&p->d_stage_nodes, node_bytes));
+    f = (C*)p->d_stage_nodes;
+  }
+  C* grid = (C*)p->d_grid;
+  rec(p, 0, 0);
+  const long long cells = p->geom.grid_cells * p->B;
+  const int nblk = (int)std::min<long long>((cells + THREADS - 1) / THREADS, (long long)p->sm_count * 16);
+  deconv_pad_kernel<T><<<nblk, THREADS, 0, p->stream>>>(p->geom, fhat, (const T*)p->d_betaT, grid);
+  ++p->launches;
+  CKL();
+  rec(p, 0, 1);
+  cufftResult r;
+  if constexpr (sizeof(T) == 8)
+    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)grid, (cufftDoubleComplex*)grid, CUFFT_FORWARD);
+  else
+    r = cufftExecC2C(p->fft, (cufftComplex*)grid, (cufftComplex*)grid, CUFFT_FORWARD);
+  if (r != CUFFT_SUCCESS) return NFFT_ERROR_CUFFT;
+  rec(p, 0, 2);
+  if (p->tiled) {
+    ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
+        p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
+  } else {
+    ks.interp_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, grid, (const T*)p->d_ks, p->d_perm,
+                                                               p->node_begin, p->node_end, f);
+  }
+  ++p->launches;
+  CKL();
+  rec(p, 0, 3);
+  if (host_out) {
+    CK(cudaMemcpyAsync(f_out, f, node_bytes, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  }
+  return NFFT_SUCCESS;
+}
+
+template <typename T>
+nfft_status adjoint_impl(nfft_plan p, const void* f_in, void* y_out) {
+  using C = typename cplx<T>::type;
+  const KernelSet<T>& ks = kernels_of<T>(p);
+  const WinPoly<T>& wp = poly_of<T>(p);
+  const size_t grid_bytes_out = (size_t)p->B * p->geom.ngrid_cells * sizeof(C);
+  const size_t node_bytes = (size_t)p->B * p->M * sizeof(C);
+  const C* f = (const C*)f_in;
+  C* y = (C*)y_out;
+  const bool host_in = !is_device_pointer(f_in);
+  const bool host_out = !is_device_pointer(y_out);
+  if (host_in) {
+    if (!p->d_stage_nodes) CK(cudaMalloc(&p->d_stage_nodes, node_bytes));
+    CK(cudaMemcpyAsync(p->d_stage_nodes, f_in, node_bytes, cudaMemcpyHostToDevice, p->stream));
+    f = (const C*)p->d_stage_nodes;
+  }
+  if (host_out) {
+    if (!p->d_stage_grid) CK(cudaMalloc(&p->d_stage_grid, grid_bytes_out));
+    y = (C*)p->d_stage_grid;
+  }
+  C* grid = (C*)p->d_grid;
+  rec(p, 1, 0);
+  const long long n16 = (long long)(p->geom.grid_cells * p->B * sizeof(C) / 16);
+  zero_kernel<<<(int)std::min<long long>((n16 + THREADS - 1) / THREADS, (long long)p->sm_count * 16), THREADS, 0,
+                p->stream>>>((float4*)grid, n16);
+  ++p->launches;
+  CKL();
+  rec(p, 1, 1);
+  if (p->tiled) {
+    ks.spread_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
+        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, grid);
+  } else {
+    ks.spread_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, f, (const T*)p->d_ks, p->d_perm,
+                                                               p->node_begin, p->node_end, grid);
+  }
+  ++p->launches;
+  CKL();
+  rec(p, 1, 2);
+  cufftResult r;
+  if constexpr (sizeof(T) == 8)
+    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)grid, (cufftDoubleComplex*)grid, CUFFT_INVERSE);
+  else
+    r = cufftExecC2C(p->fft, (cufftComplex*)grid, (cufftComplex*)grid, CUFFT_INVERSE);
+  if (r != CUFFT_SUCCESS) return NFFT_ERROR_CUFFT;
+  rec(p, 1, 3);
+  const long long outs = p->geom.ngrid_cells * p->B;
+  const int nblk = (int)std::min<long long>((outs + THREADS - 1) / THREADS, (long long)p->sm_count * 16);
+  crop_deconv_kernel<T><<<nblk, THREADS, 0, p->stream>>>(p->geom, grid, (const T*)p->d_betaT, y);
+  ++p->launches;
+  CKL();
+  rec(p, 1, 4);
+  if (host_out) {
+    CK(cudaMemcpyAsync(y_out, y, grid_bytes_out, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  }
+  return NFFT_SUCCESS;
+}
+
+nfft_status copy_nodes(nfft_plan p, const void* nodes) {
+  const size_t bytes = (size_t)p->M * p->D * p->rsize();
+  CK(cudaMemcpyAsync(p->d_nodes, nodes, bytes, is_device_pointer(nodes) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     p->stream));
+  return NFFT_SUCCESS;
+}
+
+nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, const void* nodes, double sigma, int m,
+                        nfft_window window, nfft_precision precision, const nfft_options* opt_in) {
+  if (!out || !N || !nodes) return NFFT_ERROR_INVALID_VALUE;
+  *out = nullptr;
+  if (D > 3) return NFFT_ERROR_UNSUPPORTED;
+  if (D < 1 || M < 1 || m < 1) return NFFT_ERROR_INVALID_VALUE;
+  if (window != NFFT_WINDOW_KAISER_BESSEL) return NFFT_ERROR_INVALID_VALUE;
+  if (precision != NFFT_COMPLEX64 && precision != NFFT_COMPLEX128) return NFFT_ERROR_INVALID_VALUE;
+  nfft_options opt;
+  nfft_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  if (opt.batch < 1) return NFFT_ERROR_INVALID_VALUE;
+  if (opt.method < 0 || opt.method > 2) return NFFT_ERROR_INVALID_VALUE;
+  if (!(sigma > 1.0) || !std::isfinite(sigma)) return NFFT_ERROR_BAD_GEOMETRY;
+  if (m > MAX_M) return NFFT_ERROR_UNSUPPORTED;
+  if (M > (int64_t)0x7fffffff - 1) return NFFT_ERROR_UNSUPPORTED;
+  int64_t Nt[3] = {1, 1, 1};
+  int64_t cells = 1, ncells = 1;
+  for (int d = 0; d < D; ++d) {
+    if (N[d] < 2 || (N[d] & 1)) return NFFT_ERROR_BAD_GEOMETRY;
+    if (N[d] > (int64_t)1 << 30) return NFFT_ERROR_UNSUPPORTED;
+    Nt[d] = 2 * (int64_t)std::ceil(sigma * (double)N[d] / 2.0);
+    if (2 * (int64_t)m >= Nt[d]) return NFFT_ERROR_BAD_GEOMETRY;
+    cells *= Nt[d];
+    ncells *= N[d];
+    if (cells > (int64_t)0x7fffffff) return NFFT_ERROR_UNSUPPORTED;
+  }
+  if (opt.max_subproblem < 0 || opt.max_subproblem > THREADS) return NFFT_ERROR_BAD_TILE;
+  const int64_t nend = opt.node_end == 0 ? M : opt.node_end;
+  if (opt.node_begin < 0 || opt.node_begin > nend || nend > M) return NFFT_ERROR_INVALID_VALUE;
+  // tiles: defaults sized so the tile region fits shared memory with >= 2 CTAs/SM
+  const bool c128 = precision == NFFT_COMPLEX128;
+  const size_t csz = c128 ? 16 : 8;
+  int64_t Q[3] = {1, 1, 1}, P[3] = {1, 1, 1};
+  for (int d = 0; d < D; ++d) {
+    int64_t q = opt.tile[d];
+    if (q < 0 || q > Nt[d]) return NFFT_ERROR_BAD_TILE;
+    if (q == 0) q = D == 1 ? 512 : (D == 2 ? 32 : 8);
+    q = std::min<int64_t>(q, Nt[d]);
+    Q[d] = q;
+    P[d] = (Nt[d] + q - 1) / q;
+  }
+  size_t region_cells = 1;
+  for (int d = 0; d < D; ++d) region_cells *= (size_t)(Q[d] + 2 * m - 1);
+  const size_t region_bytes = region_cells * csz;
+
+  DeviceGuard guard(opt.device);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  const size_t smem_max = prop.sharedMemPerBlockOptin;
+  bool tiled;
+  if (opt.method == NFFT_METHOD_TILED) {
+    if (region_bytes > smem_max) return NFFT_ERROR_BAD_TILE;
+    tiled = true;
+  } else if (opt.method == NFFT_METHOD_DIRECT) {
+    tiled = false;
+  } else {
+    tiled = region_bytes <= smem_max;
+  }
+
+  nfft_plan p = new (std::nothrow) nfft_plan_s();
+  if (!p) return NFFT_ERROR_OUT_OF_MEMORY;
+  p->D = D;
+  p->M = M;
+  p->B = opt.batch;
+  p->m = m;
+  p->sigma = sigma;
+  p->prec = precision;
+  p->opt = opt;
+  p->device = dev;
+  p->stream = (cudaStream_t)opt.stream;
+  p->sm_count = prop.multiProcessorCount;
+  p->tiled = tiled;
+  p->S = opt.max_subproblem > 0 ? (int)opt.max_subproblem : THREADS;
+  p->node_begin = (int)opt.node_begin;
+  p->node_end = (int)nend;
+  p->region_bytes = region_bytes;
+  p->deg = poly_degree(m, c128);
+  int64_t n_tiles = 1;
+  for (int d = 0; d < D; ++d) {
+    p->N[d] = N[d];
+    p->Nt[d] = Nt[d];
+    p->Q[d] = Q[d];
+    p->P[d] = P[d];
+    p->beta[d] = M_PI * m * (2.0 - (double)N[d] / (double)Nt[d]);  // reading R4
+    n_tiles *= P[d];
+  }
+  p->n_tiles = n_tiles;
+  p->nbits = 0;
+  while (((int64_t)1 << p->nbits) < n_tiles) ++p->nbits;
+  p->sort_blocks = (int)((M + SORT_TILE - 1) / SORT_TILE);
+  p->max_subs = (int)std::min<int64_t>((nend - opt.node_begin + p->S - 1) / p->S + n_tiles, 0x7fffffff);
+  if (p->max_subs < 1) p->max_subs = 1;
+
+  Geom& g = p->geom;
+  memset(&g, 0, sizeof(g));
+  g.D = D;
+  g.M = (int)M;
+  g.B = (int)p->B;
+  g.m = m;
+  int boff = 0;
+  for (int d = 0; d < MAX_D; ++d) {
+    const bool act = d < D;
+    g.Nt[d] = act ? (int)Nt[d] : 1;
+    g.N[d] = act ? (int)N[d] : 1;
+    g.Q[d] = act ? (int)Q[d] : 1;
+    g.P[d] = act ? (int)P[d] : 1;
+    g.L[d] = act ? (int)(Q[d] + 2 * m - 1) : 1;
+    g.Ntd[d] = act ? (double)Nt[d] : 1.0;
+    g.beta_off[d] = boff;
+    if (act) boff += (int)N[d];
+  }
+  g.grid_cells = cells;
+  g.ngrid_cells = ncells;
+  g.region_cells = (int)region_cells;
+
+  nfft_status st = NFFT_SUCCESS;
+  auto fail = [&](nfft_status s) {
+    free_all(p);
+    delete p;
+    return s;
+  };
+  auto alloc = [&](void** ptr, size_t bytes) -> bool {
+    if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  };
+  const size_t rs = c128 ? 8 : 4;
+  bool ok = alloc(&p->d_nodes, (size_t)M * D * rs) && alloc(&p->d_ks, (size_t)M * D * rs) &&
+            alloc((void**)&p->d_keys_a, M * 4) && alloc((void**)&p->d_vals_a, M * 4) &&
+            alloc((void**)&p->d_keys_b, M * 4) && alloc((void**)&p->d_vals_b, M * 4) &&
+            alloc((void**)&p->d_offsets, (n_tiles + 1) * 4) && alloc((void**)&p->d_hist, 256 * p->sort_blocks * 4) &&
+            alloc((void**)&p->d_scan_tmp, scan_tmp_ints(std::max<int64_t>(256 * p->sort_blocks, n_tiles + 1)) * 4) &&
+            alloc((void**)&p->d_subbase, (n_tiles + 1) * 4) && alloc((void**)&p->d_subs, (size_t)p->max_subs * 16) &&
+            alloc((void**)&p->d_err, 16) && alloc(&p->d_grid, (size_t)cells * p->B * csz) &&
+            alloc((void**)&p->d_beta64, boff * 8) && alloc(&p->d_betaT, boff * rs) &&
+            alloc((void**)&p->d_poly, (size_t)D * 2 * m * MAX_Z * 8);
+  if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
+
+  int n[3];
+  for (int d = 0; d < D; ++d) n[d] = (int)Nt[d];
+  if (cufftPlanMany(&p->fft, D, n, nullptr, 1, 0, nullptr, 1, 0, c128 ? CUFFT_Z2Z : CUFFT_C2C, (int)p->B) !=
+      CUFFT_SUCCESS)
+    return fail(NFFT_ERROR_CUFFT);
+  p->fft_ok = true;
+  if (cufftSetStream(p->fft, p->stream) != CUFFT_SUCCESS) return fail(NFFT_ERROR_CUFFT);
+
+  if (opt.timing) {
+    for (auto& row : p->ev)
+      for (auto& e : row)
+        if (cudaEventCreate(&e) != cudaSuccess) return fail(NFFT_ERROR_CUDA);
+    p->events = true;
+  }
+  if (c128) {
+    p->k64 = kernels_for<double>(D, m);
+    st = build_window_tables<double>(p);
+    if (st == NFFT_SUCCESS) st = configure_kernels<double>(p, p->k64);
+  } else {
+    p->k32 = kernels_for<float>(D, m);
+    st = build_window_tables<float>(p);
+    if (st == NFFT_SUCCESS) st = configure_kernels<float>(p, p->k32);
+  }
+  if (st == NFFT_SUCCESS) st = copy_nodes(p, nodes);
+  if (st == NFFT_SUCCESS) {
+    cudaError_t e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) {
+      last_cuda_error = e;
+      st = NFFT_ERROR_CUDA;
+    }
+  }
+  if (st != NFFT_SUCCESS) return fail(st);
+  *out = p;
+  return NFFT_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+nfft_status nfft_default_options(nfft_options* opt) {
+  if (!opt) return NFFT_ERROR_INVALID_VALUE;
+  memset(opt, 0, sizeof(*opt));
+  opt->batch = 1;
+  opt->device = -1;
+  opt->method = NFFT_METHOD_AUTO;
+  opt->check_nodes = 1;
+  return NFFT_SUCCESS;
+}
+
+nfft_status nfft_plan_create(nfft_plan* out, int D, const int64_t* N, int64_t M, const void* nodes, double sigma, int m,
+                             nfft_window window, nfft_precision precision) {
+  return create_impl(out, D, N, M, nodes, sigma, m, window, precision, nullptr);
+}
+
+nfft_status nfft_plan_create_ex(nfft_plan* out, int D, const int64_t* N, int64_t M, const void* nodes, double sigma,
+                                int m, nfft_window window, nfft_precision precision, const nfft_options* opt) {
+  return create_impl(out, D, N, M, nodes, sigma, m, window, precision, opt);
+}
+
+nfft_status nfft_set_nodes(nfft_plan p, const void* nodes) {
+  if (!p || !nodes) return NFFT_ERROR_INVALID_VALUE;
+  DeviceGuard guard(p->device);
+  nfft_status s = copy_nodes(p, nodes);
+  if (s == NFFT_SUCCESS) p->precomputed = false;
+  return s;
+}
+
+nfft_status nfft_precompute(nfft_plan p) {
+  if (!p) return NFFT_ERROR_INVALID_VALUE;
+  DeviceGuard guard(p->device);
+  nfft_status s = p->prec == NFFT_COMPLEX128 ? precompute_impl<double>(p) : precompute_impl<float>(p);
+  if (s != NFFT_SUCCESS) return s;
+  if (p->opt.check_nodes) {
+    int err = 0;
+    CK(cudaMemcpyAsync(&err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    if (err) {
+      p->precomputed = false;
+      return NFFT_ERROR_NONFINITE_NODE;
+    }
+  }
+  p->precomputed = true;
+  return NFFT_SUCCESS;
+}
+
+nfft_status nfft_forward(nfft_plan p, const void* fhat_grid, void* f_nodes) {
+  if (!p || !fhat_grid || !f_nodes) return NFFT_ERROR_INVALID_VALUE;
+  if (!p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
+  DeviceGuard guard(p->device);
+  return p->prec == NFFT_COMPLEX128 ? forward_impl<double>(p, fhat_grid, f_nodes)
+                                    : forward_impl<float>(p, fhat_grid, f_nodes);
+}
+
+nfft_status nfft_adjoint(nfft_plan p, const void* f_nodes, void* fhat_grid) {
+  if (!p || !fhat_grid || !f_nodes) return NFFT_ERROR_INVALID_VALUE;
+  if (!p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
+  DeviceGuard guard(p->device);
+  return p->prec == NFFT_COMPLEX128 ? adjoint_impl<double>(p, f_nodes, fhat_grid)
+                                    : adjoint_impl<float>(p, f_nodes, fhat_grid);
+}
+
+nfft_status nfft_plan_destroy(nfft_plan p) {
+  if (!p) return NFFT_ERROR_INVALID_VALUE;
+  DeviceGuard guard(p->device);
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  free_all(p);
+  delete p;
+  if (e != cudaSuccess) {
+    last_cuda_error = e;
+    return NFFT_ERROR_CUDA;
+  }
+  return NFFT_SUCCESS;
+}
+
+const char* nfft_status_string(nfft_status s) {
+  switch (s) {
+    case NFFT_SUCCESS: return "success";
+    case NFFT_ERROR_INVALID_VALUE: return "invalid value";
+    case NFFT_ERROR_BAD_GEOMETRY: return "bad geometry (N_d even >= 2, sigma > 1, 2m < Ntilde_d)";
+    case NFFT_ERROR_NONFINITE_NODE: return "non-finite node coordinate";
+    case NFFT_ERROR_BAD_TILE: return "bad tile size";
+    case NFFT_ERROR_NOT_PRECOMPUTED: return "plan not precomputed";
+    case NFFT_ERROR_OUT_OF_MEMORY: return "out of device memory";
+    case NFFT_ERROR_CUDA: return last_cuda_error != cudaSuccess ? cudaGetErrorString(last_cuda_error) : "CUDA error";
+    case NFFT_ERROR_CUFFT: return "cuFFT error";
+    case NFFT_ERROR_UNSUPPORTED: return "unsupported (D > 3, m > 8, or size beyond int32 indexing)";
+  }
+  return "unknown status";
+}
+
+nfft_status nfft_plan_info(nfft_plan p, int64_t* Ntilde, int64_t* tile, int64_t* tiles_per_dim, int64_t* n_tiles) {
+  if (!p) return NFFT_ERROR_INVALID_VALUE;
+  for (int d = 0; d < p->D; ++d) {
+    if (Ntilde) Ntilde[d] = p->Nt[d];
+    if (tile) tile[d] = p->Q[d];
+    if (tiles_per_dim) tiles_per_dim[d] = p->P[d];
+  }
+  if (n_tiles) *n_tiles = p->n_tiles;
+  return NFFT_SUCCESS;
+}
+
+nfft_status nfft_get_binning(nfft_plan p, int32_t* perm_host, int32_t* offsets_host) {
+  if (!p) return NFFT_ERROR_INVALID_VALUE;
+  if (!p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
+  DeviceGuard guard(p->device);
+  if (perm_host) CK(cudaMemcpyAsync(perm_host, p->d_perm, p->M * 4, cudaMemcpyDeviceToHost, p->stream));
+  if (offsets_host)
+    CK(cudaMemcpyAsync(offsets_host, p->d_offsets, (p->n_tiles + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return NFFT_SUCCESS;
+}
+
+nfft_status nfft_get_window_tables(nfft_plan p, double* beta_tensor, double* poly, int* deg) {
+  if (!p) return NFFT_ERROR_INVALID_VALUE;
+  DeviceGuard guard(p->device);
+  int64_t nb = 0;
+  for (int d = 0; d < p->D; ++d) nb += p->N[d];
+  if (beta_tensor) CK(cudaMemcpyAsync(beta_tensor, p->d_beta64, nb * 8, cudaMemcpyDeviceToHost, p->stream));
+  if (poly) {
+    const int Z = p->deg + 1;
+    const size_t cnt = (size_t)p->D * 2 * p->m;
+    double* tmp = new (std::nothrow) double[cnt * MAX_Z];
+    if (!tmp) return NFFT_ERROR_OUT_OF_MEMORY;
+    cudaError_t e = cudaMemcpyAsync(tmp, p->d_poly, cnt * MAX_Z * 8, cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) {
+      delete[] tmp;
+      last_cuda_error = e;
+      return NFFT_ERROR_CUDA;
+    }
+    for (size_t r = 0; r < cnt; ++r)
+      for (int z = 0; z < Z; ++z) poly[r * Z + z] = tmp[r * MAX_Z + z];
+    delete[] tmp;
+  }
+  if (deg) *deg = p->deg;
+  CK(cudaStreamSynchronize(p->stream));
+  return NFFT_SUCCESS;
+}
+
+nfft_status nfft_get_stage_times(nfft_plan p, int which, float* ms) {
+  if (!p || !ms || which < 0 || which > 1) return NFFT_ERROR_INVALID_VALUE;
+  if (!p->events) return NFFT_ERROR_INVALID_VALUE;
+  DeviceGuard guard(p->device);
+  CK(cudaStreamSynchronize(p->stream));
+  for (int i = 0; i < 5; ++i) ms[i] = 0.f;
+  auto el = [&](int w, int a, int b) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, p->ev[w][a], p->ev[w][b]) != cudaSuccess) {
+      cudaGetLastError();
+      t = 0.f;
+    }
+    return t;
+  };
+  if (which == 0) {
+    ms[0] = el(0, 0, 1);
+    ms[1] = el(0, 1, 2);
+    ms[2] = el(0, 2, 3);
+  } else {
+    ms[3] = el(1, 0, 1);
+    ms[2] = el(1, 1, 2);
+    ms[1] = el(1, 2, 3);
+    ms[0] = el(1, 3, 4);
+  }
+  ms[4] = el(2, 0, 1);
+  return NFFT_SUCCESS;
+}
+
+nfft_status nfft_get_launch_count(nfft_plan p, int64_t* launches) {
+  if (!p || !launches) return NFFT_ERROR_INVALID_VALUE;
+  *launches = p->launches;
+  return NFFT_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.
+
+Bars (BASELINE.json north_star): relative l2 <= 1e-12 for ComplexF64 and
+<= 2e-5 for ComplexF32; the node binning / sort permutation bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import binning as obin
+from oracle import nfft as onfft
+from oracle import window as owin
+from paper_2208_00049_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-12, "c64": 2e-5}
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _plan(w, **kw):
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    nodes = torch.from_numpy(np.ascontiguousarray(w["nodes"])).cuda()
+    return pkg.NfftPlan(nodes, w["N"], m=w["m"], sigma=w["sigma"], precision=w["precision"],
+                        batch=w["batch"], **kw).precompute()
+
+
+def _run(w, **kw):
+    torch = _torch()
+    plan = _plan(w, **kw)
+    fhat = torch.from_numpy(w["fhat"]).cuda()
+    f = torch.from_numpy(w["f"]).cuda()
+    got_f = plan.forward(fhat).cpu().numpy()
+    got_y = plan.adjoint(f).cpu().numpy()
+    info = plan.info()
+    plan.close()
+    return got_f, got_y, info
+
+
+def _oracle(w, batches=None):
+    bs = range(w["batch"]) if batches is None else batches
+    nodes = w["nodes"].astype(np.float64)
+    rf = np.stack([onfft.forward(nodes, w["fhat"][b].astype(np.complex128), w["N"], w["m"], w["sigma"]) for b in bs])
+    ry = np.stack([onfft.adjoint(nodes, w["f"][b].astype(np.complex128), w["N"], w["m"], w["sigma"]) for b in bs])
+    return rf, ry
+
+
+def _check(w, tol=None, **kw):
+    tol = tol or TOL[w["precision"]]
+    got_f, got_y, info = _run(w, **kw)
+    rf, ry = _oracle(w)
+    for b in range(w["batch"]):
+        ef, ey = rel_l2(got_f[b], rf[b]), rel_l2(got_y[b], ry[b])
+        assert ef <= tol and ey <= tol, (b, ef, ey, info)
+    return info
+
+
+# ------------------------------------------------------------------ binning
+
+@pytest.mark.parametrize("config", ["cfg1_1d_256", "cfg2_1d_2e18", "cfg3_2d_512", "cfg4_3d_64",
+                                    "cfg5_radial_s2", "cfg5_radial_s125"])
+def test_binning_bit_exact_on_configs(config):
+    w = workloads.make(config, seed=0, batch=1)
+    plan = _plan(w)
+    perm, offs = plan.binning()
+    info = plan.info()
+    plan.close()
+    ref_perm, ref_offs, P = obin.bin_nodes(w["nodes"], info["Ntilde"], info["tile"])
+    assert tuple(info["tiles_per_dim"]) == P
+    np.testing.assert_array_equal(perm, ref_perm)
+    np.testing.assert_array_equal(offs, ref_offs)
+
+
+@pytest.mark.parametrize("tile", [(7,), (1,), (400,)])
+def test_binning_edge_nodes_1d(tile):
+    """On-grid nodes, k = +1/2 (folds to -1/2), out-of-range nodes (periodic
+    fold), coincident nodes, ragged last tile, single tile, one-cell tiles."""
+    N = 200
+    rng = np.random.default_rng(3)
+    nodes = np.concatenate([np.arange(-N, N) / (2 * N),          # every grid point (Ntilde = 400)
+                            [0.5, -0.5, 0.0, 0.0, 0.0, 1.25, -3.7, 2.0 - 1e-17],
+                            rng.random(300) - 0.5])[:, None]
+    w = dict(nodes=nodes, N=(N,), m=3, sigma=2.0, precision="c128", batch=1)
+    plan = _plan(w, tile=tile)
+    perm, offs = plan.binning()
+    info = plan.info()
+    plan.close()
+    ref_perm, ref_offs, _ = obin.bin_nodes(nodes, info["Ntilde"], info["tile"])
+    np.testing.assert_array_equal(perm, ref_perm)
+    np.testing.assert_array_equal(offs, ref_offs)
+
+
+def test_binning_all_nodes_one_tile_and_many_tiles():
+    """Degenerate partitions: 4096 identical nodes (one hot tile) and
+    2^16 tiles in 2D (more radix passes)."""
+    nodes = np.zeros((4096, 2)) + 0.1234
+    w = dict(nodes=nodes, N=(256, 256), m=4, sigma=2.0, precision="c128", batch=1)
+    plan = _plan(w, tile=(2, 2))
+    perm, offs = plan.binning()
+    info = plan.info()
+    plan.close()
+    assert info["n_tiles"] == 256 * 256
+    ref_perm, ref_offs, _ = obin.bin_nodes(nodes, info["Ntilde"], info["tile"])
+    np.testing.assert_array_equal(perm, ref_perm)
+    np.testing.assert_array_equal(offs, ref_offs)
+
+
+# ------------------------------------------------------------------ window tables
+
+@pytest.mark.parametrize("m", [2, 4, 8])
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_window_tables_against_oracle_window(m, precision):
+    """beta^tensor = 1/(m phi_Base(m n/Ntilde)) and the
+    polynomial taps against the exact truncated window psi_hat_Base."""
+    N = (100, 64)
+    w = dict(nodes=np.zeros((1, 2)), N=N, m=m, sigma=2.0, precision=precision, batch=1)
+    plan = _plan(w)
+    beta_t, poly, deg = plan.window_tables()
+    plan.close()
+    off = 0
+    for d, n in enumerate(N):
+        nt = 2 * n
+        b = owin.kb_beta(m, 2.0)
+        nn = np.arange(-(n // 2), n // 2)
+        ref = 1.0 / (m * owin.phi_base(m * nn / nt, b))
+        assert np.max(np.abs(beta_t[off:off + n] - ref) / ref) < 1e-14
+        off += n
+        zeta = np.linspace(-0.5, 0.5, 1001)[:-1]
+        peak = owin.psi_hat_base(np.array([0.0]), b)[0]
+        for l in range(2 * m):
+            exact = owin.psi_hat_base((zeta + 0.5 + m - 1 - l) / m, b)
+            approx = np.polyval(poly[d, l, ::-1], zeta)
+            err = np.max(np.abs(approx - exact)) / peak
+            assert err < (1e-13 if precision == "c128" else 2e-7), (d, l, err)
+
+
+# ------------------------------------------------------------------ forward / adjoint parity
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("method", ["tiled", "direct"])
+def test_config1_all_m(m, method):
+    """BASELINE configs[0] (1D N=256, M=256) at every compiled m; ragged tiles."""
+    w = workloads.make("cfg1_1d_256", seed=0, m=m)
+    _check(w, method=method, tile=(96,))
+
+
+@pytest.mark.parametrize("method", ["tiled", "direct"])
+@pytest.mark.parametrize("m", [3, 4, 8])
+def test_2d_small_ragged_tiles(method, m):
+    w = workloads.make("cfg3_2d_512", seed=1, N=(48, 40), M=3000, m=m)
+    _check(w, method=method, tile=(20, 14))
+
+
+@pytest.mark.parametrize("method", ["tiled", "direct"])
+@pytest.mark.parametrize("m", [2, 4, 5])
+def test_3d_small_ragged_tiles(method, m):
+    w = workloads.make("cfg4_3d_64", seed=2, N=(16, 12, 10), M=2000, m=m)
+    _check(w, method=method, tile=(6, 5, 7))
+
+
+@pytest.mark.parametrize("D", [1, 2, 3])
+def test_batch_and_c64(D):
+    N = {1: (300,), 2: (40, 36), 3: (12, 12, 10)}[D]
+    w = workloads.make({1: "cfg2_1d_2e18", 2: "cfg3_2d_512", 3: "cfg4_3d_64"}[D], seed=3, N=N, M=1500, m=4, batch=3)
+    _check(w)
+    w32 = dict(w, nodes=w["nodes"].astype(np.float32), fhat=w["fhat"].astype(np.complex64),
+               f=w["f"].astype(np.complex64), precision="c64")
+    _check(w32)
+
+
+def test_edge_cases_m1_node_one_cell_tiles_and_wrap():
+    """M = 1; nodes at the torus boundary and outside [-1/2,1/2); 1-cell tiles."""
+    w = dict(nodes=np.array([[0.5 - 1e-16, -0.5]]), N=(8, 6), m=2, sigma=2.0, precision="c128", batch=1,
+             fhat=workloads.complex_normal(np.random.default_rng(0), (1, 8, 6)), f=np.array([[1.0 - 2.0j]]))
+    _check(w, tile=(1, 1))
+    nodes = np.array([[0.5, 0.5], [-0.5, 0.25], [1.75, -2.3], [0.0, 0.0], [0.0, 0.0], [0.125, -0.25]])
+    w = dict(w, nodes=nodes, f=workloads.complex_normal(np.random.default_rng(1), (1, 6)), N=(16, 20), m=4)
+    _check(w, tile=(3, 5))
+    _check(w, method="direct")
+
+
+@pytest.mark.parametrize("config,ms", [("cfg2_1d_2e18", [3, 4, 8]), ("cfg3_2d_512", [3, 4, 8]), ("cfg4_3d_64", [4])])
+def test_full_size_configs(config, ms):
+    """BASELINE configs[1..3] at full size in the bench's launch configuration."""
+    for m in ms:
+        w = workloads.make(config, seed=0, m=m)
+        _check(w)
+
+
+@pytest.mark.parametrize("config", ["cfg5_radial_s2", "cfg5_radial_s125"])
+def test_radial_batch_c64_sampled(config):
+    """BASELINE configs[4]: radial, B = 32, ComplexF32; the oracle checks three
+    of the 32 vectors (same launch as the bench: all 32 computed)."""
+    w = workloads.make(config, seed=0)
+    got_f, got_y, _ = _run(w)
+    bs = [0, 17, 31]
+    rf, ry = _oracle(w, bs)
+    for i, b in enumerate(bs):
+        assert rel_l2(got_f[b], rf[i]) <= 2e-5
+        assert rel_l2(got_y[b], ry[i]) <= 2e-5
+
+
+# ------------------------------------------------------------------ invariants / API paths
+
+def test_adjoint_identity_on_gpu():
+    torch = _torch()
+    w = workloads.make("cfg3_2d_512", seed=5, N=(64, 64), M=5000, m=5)
+    plan = _plan(w)
+    Af = plan.forward(torch.from_numpy(w["fhat"]).cuda()).cpu().numpy()[0]
+    AHf = plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()[0]
+    plan.close()
+    lhs = np.vdot(w["f"][0], Af)
+    rhs = np.vdot(AHf, w["fhat"][0])
+    assert abs(lhs - rhs) / (np.linalg.norm(Af) * np.linalg.norm(w["f"][0])) < 1e-14
+
+
+def test_host_pointer_path_matches_device_path():
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    w = workloads.make("cfg3_2d_512", seed=6, N=(32, 48), M=1000, m=4)
+    dev_f, dev_y, _ = _run(w)
+    plan = pkg.NfftPlan(w["nodes"], w["N"], m=4).precompute()   # numpy nodes (host)
+    host_f = plan.forward(w["fhat"])                              # numpy in -> numpy out
+    host_y = plan.adjoint(w["f"])
+    plan.close()
+    assert isinstance(host_f, np.ndarray)
+    np.testing.assert_array_equal(host_f, dev_f)
+    assert rel_l2(host_y, dev_y) < 1e-15
+
+
+def test_shards_sum_to_full_transform():
+    """Linearity: adjoints of disjoint shards of the
+    sorted order sum to the full adjoint; forward shards write their nodes."""
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    from paper_2208_00049_b200 import dist
+    w = workloads.make("cfg3_2d_512", seed=7, N=(64, 64), M=6000, m=4)
+    full_f, full_y, _ = _run(w)
+    nodes = torch.from_numpy(w["nodes"]).cuda()
+    acc = np.zeros_like(full_y)
+    seen = np.zeros(w["M"], bool)
+    for rank in range(3):
+        rng = dist.shard_range(w["M"], rank, 3)
+        plan = pkg.NfftPlan(nodes, w["N"], m=4, node_range=rng).precompute()
+        perm, _ = plan.binning()
+        out = torch.zeros((1, w["M"]), dtype=torch.complex128, device="cuda")
+        plan.forward(torch.from_numpy(w["fhat"]).cuda(), out=out)
+        mine = perm[rng[0]:rng[1]]
+        np.testing.assert_array_equal(out.cpu().numpy()[0, mine], full_f[0, mine])
+        seen[mine] = True
+        acc += plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
+        plan.close()
+    assert seen.all()
+    assert rel_l2(acc, full_y) < 1e-14
+
+
+def test_errors_are_reported():
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    nodes = torch.tensor([[0.1, float("nan")]], dtype=torch.float64, device="cuda")
+    plan = pkg.NfftPlan(nodes, (16, 16), m=2)
+    with pytest.raises(pkg.NfftError) as e:
+        plan.forward(torch.zeros((1, 16, 16), dtype=torch.complex128, device="cuda"))
+    assert e.value.name == "NFFT_ERROR_NOT_PRECOMPUTED"
+    with pytest.raises(pkg.NfftError) as e:
+        plan.precompute()
+    assert e.value.name == "NFFT_ERROR_NONFINITE_NODE"
+    plan.close()
+    with pytest.raises(pkg.NfftError) as e:
+        pkg.NfftPlan(torch.zeros((4, 2), dtype=torch.float64, device="cuda"), (16, 16), m=2, tile=(40, 4))
+    assert e.value.name == "NFFT_ERROR_BAD_TILE"
+    with pytest.raises(pkg.NfftError) as e:
+        pkg.NfftPlan(torch.zeros((4, 1), dtype=torch.float64, device="cuda"), (8,), m=8)
+    assert e.value.name == "NFFT_ERROR_BAD_GEOMETRY"
