@@ -183,7 +183,8 @@ def test_edge_cases_m1_node_one_cell_tiles_and_wrap():
              fhat=workloads.complex_normal(np.random.default_rng(0), (1, 8, 6)), f=np.array([[1.0 - 2.0j]]))
     _check(w, tile=(1, 1))
     nodes = np.array([[0.5, 0.5], [-0.5, 0.25], [1.75, -2.3], [0.0, 0.0], [0.0, 0.0], [0.125, -0.25]])
-    w = dict(w, nodes=nodes, f=workloads.complex_normal(np.random.default_rng(1), (1, 6)), N=(16, 20), m=4)
+    w = dict(w, nodes=nodes, f=workloads.complex_normal(np.random.default_rng(1), (1, 6)), N=(16, 20), m=4,
+             fhat=workloads.complex_normal(np.random.default_rng(2), (1, 16, 20)))
     _check(w, tile=(3, 5))
     _check(w, method="direct")
 
