@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true", help="skip the m = 3..8 sweep lines")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline measurement")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step kernel by kernel (no CUDA graph)")
     return ap.parse_args()
 
 
@@ -261,56 +262,81 @@ def main():
             p.precompute()
             return p, p, nodes
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_r = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
 
-    def run_steps(wk, steps, warmup, timing=True):
-        obj, plan, nodes = build_plan(wk, timing)
+    class _Flush:
+        """L2 flush between steps: write 256 MiB (> 126 MB L2), then read another
+        256 MiB so the write-back of the dirty lines also happens here and not
+        inside the next timed step."""
+        @staticmethod
+        def zero_():
+            flush_w.zero_()
+            flush_sink.copy_(flush_r.sum())
+    flush = _Flush()
+
+    def run_steps(wk, steps, warmup, use_graph=not a.no_graph):
+        """K timed steps; each stage of the step is its own CUDA graph (or plain
+        launches with --no-graph) bracketed by CUDA events on the plan stream, so
+        the step time and every stage time are measured live."""
+        obj, plan, nodes = build_plan(wk, False)
         with torch.cuda.stream(stream):
             fhat = torch.from_numpy(wk["fhat"]).to(dev)
             f = torch.from_numpy(wk["f"]).to(dev)
-            fout = torch.empty((wk["batch"], wk["M"]), dtype=plan.tdtype_c, device=dev)
+            fout = torch.zeros((wk["batch"], wk["M"]), dtype=plan.tdtype_c, device=dev)
             yout = torch.empty((wk["batch"],) + tuple(wk["N"]), dtype=plan.tdtype_c, device=dev)
         stream.synchronize()
-
-        def step():
-            plan.precompute()
-            obj.forward(fhat, out=fout)
-            obj.adjoint(f, out=yout)
-
+        shard = a.mode == "nodeshard"
+        from paper_2208_00049_b200.dist import allreduce_sum
+        stages = [("precompute", lambda: plan.run_stage("precompute")),
+                  ("deconv", lambda: plan.run_stage("fwd_deconv", fhat)),
+                  ("fft_fwd", lambda: plan.run_stage("fwd_fft")),
+                  ("interp", lambda: plan.run_stage("fwd_interp", None, fout))]
+        if shard:
+            stages.append(("allreduce_fwd", lambda: allreduce_sum(fout)))
+        stages += [("spread", lambda: plan.run_stage("adj_spread", f)),
+                   ("fft_adj", lambda: plan.run_stage("adj_fft")),
+                   ("crop", lambda: plan.run_stage("adj_crop", None, yout))]
+        if shard:
+            stages.append(("allreduce_adj", lambda: allreduce_sum(yout)))
         for _ in range(warmup):
             with torch.cuda.stream(stream):
                 flush.zero_()
-                step()
+                for _, fn in stages:
+                    fn()
         stream.synchronize()
-        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-        stage = {"precompute": [], "deconv": [], "fft_fwd": [], "interp": [], "zero": [], "spread": [],
-                 "fft_adj": [], "crop": []}
+        runs, launches_per_step, graphs = [], 0, []
+        for name, fn in stages:
+            if use_graph:
+                g = torch.cuda.CUDAGraph()
+                l0 = plan.launches()
+                with torch.cuda.graph(g, stream=stream):
+                    fn()
+                launches_per_step += plan.launches() - l0
+                graphs.append(g)
+                runs.append((name, g.replay))
+            else:
+                runs.append((name, fn))
+        stream.synchronize()
         l0 = plan.launches()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(runs) + 1)] for _ in range(steps)]
         barrier()
         torch.cuda.synchronize(dev)
         with ClockSampler(local) as clk:
             for s in range(steps):
                 with torch.cuda.stream(stream):
                     flush.zero_()
-                    ev0[s].record(stream)
-                    step()
-                    ev1[s].record(stream)
-                if timing:
-                    tf = plan.stage_times("forward")   # synchronises the plan stream
-                    ta = plan.stage_times("adjoint")
-                    stage["precompute"].append(tf["precompute"])
-                    stage["deconv"].append(tf["deconv"])
-                    stage["fft_fwd"].append(tf["fft"])
-                    stage["interp"].append(tf["resample"])
-                    stage["zero"].append(ta["zero"])
-                    stage["spread"].append(ta["resample"])
-                    stage["fft_adj"].append(ta["fft"])
-                    stage["crop"].append(ta["deconv"])
+                    for k, (_, fn) in enumerate(runs):
+                        ev[s][k].record(stream)
+                        fn()
+                    ev[s][len(runs)].record(stream)
             torch.cuda.synchronize(dev)
         barrier()
-        launches = plan.launches() - l0
-        ms = sum(e0.elapsed_time(e1) for e0, e1 in zip(ev0, ev1))
+        launches = launches_per_step * steps if use_graph else plan.launches() - l0
+        stage = {name: [ev[s][k].elapsed_time(ev[s][k + 1]) for s in range(steps)] for k, (name, _) in enumerate(runs)}
+        ms = sum(ev[s][0].elapsed_time(ev[s][len(runs)]) for s in range(steps))
+        del graphs
         obj.close()
         return ms, stage, launches, clk.summary()
 
@@ -326,10 +352,10 @@ def main():
     # roofline of the dominant library kernel (by mean share of the step)
     alg = algorithmic(w)
     means = {k: (statistics.mean(v) if v else 0.0) for k, v in stage.items()}
-    mine = {k: v for k, v in means.items() if not k.startswith("fft")}
+    mine = {k: v for k, v in means.items() if not k.startswith("fft") and not k.startswith("allreduce")}
     dom = max(mine, key=mine.get)
     bytes_of = {"interp": alg["resample_bytes"], "spread": alg["resample_bytes"], "deconv": alg["deconv_bytes"],
-                "crop": alg["crop_bytes"], "zero": alg["zero_bytes"],
+                "crop": alg["crop_bytes"], "allreduce_fwd": 0, "allreduce_adj": 0,
                 "precompute": (8 * len(w["N"]) + 4 * 6) * w["M"]}
     flops_of = {"interp": alg["resample_flops"], "spread": alg["resample_flops"]}
     fp64 = w["precision"] == "c128"

@@ -67,7 +67,8 @@ typedef enum {
 typedef enum {
   NFFT_METHOD_AUTO = 0,   /* tiled when the tile+halo fits shared memory */
   NFFT_METHOD_TILED = 1,  /* Alg. 3/4: grid tile + m-halo staged in shared memory */
-  NFFT_METHOD_DIRECT = 2  /* unblocked resampling straight from L2/HBM */
+  NFFT_METHOD_DIRECT = 2, /* unblocked resampling straight from L2/HBM */
+  NFFT_METHOD_TILED_CAS = 3 /* tiled, adjoint with shared-memory atomics (reference variant) */
 } nfft_method;
 
 typedef struct {
@@ -121,6 +122,26 @@ nfft_status nfft_forward(nfft_plan p, const void* fhat_grid, void* f_nodes);
 /* Adjoint NFFT, Alg. 2: f_nodes (B, M) -> fhat_grid (B, N...).
  * Only nodes of the plan's shard contribute (linearity: shards sum). */
 nfft_status nfft_adjoint(nfft_plan p, const void* f_nodes, void* fhat_grid);
+
+/*
+ * The three steps of Alg. 1 / Alg. 2 as separately launchable stages, for
+ * callers that overlap or time them (each enqueues only its own kernels on the
+ * plan stream; all data pointers must be DEVICE pointers, else
+ * NFFT_ERROR_INVALID_VALUE). nfft_forward = FWD_DECONV, FWD_FFT, FWD_INTERP;
+ * nfft_adjoint = ADJ_SPREAD, ADJ_FFT, ADJ_CROP. The oversampled grid between
+ * stages is plan scratch. NFFT_STAGE_PRECOMPUTE is nfft_precompute without
+ * the node check (fully asynchronous; CUDA-graph capturable).
+ */
+typedef enum {
+  NFFT_STAGE_PRECOMPUTE = 0,  /* in, out unused */
+  NFFT_STAGE_FWD_DECONV = 1,  /* in: fhat_grid (B, N...) -> scratch grid */
+  NFFT_STAGE_FWD_FFT = 2,     /* scratch grid, e^{-2 pi i}, unnormalised */
+  NFFT_STAGE_FWD_INTERP = 3,  /* scratch grid -> out: f_nodes (B, M) */
+  NFFT_STAGE_ADJ_SPREAD = 4,  /* in: f_nodes (B, M) -> scratch grid */
+  NFFT_STAGE_ADJ_FFT = 5,     /* scratch grid, e^{+2 pi i}, unnormalised */
+  NFFT_STAGE_ADJ_CROP = 6     /* scratch grid -> out: fhat_grid (B, N...) */
+} nfft_stage;
+nfft_status nfft_run_stage(nfft_plan p, int stage, const void* in, void* out);
 
 nfft_status nfft_plan_destroy(nfft_plan p);
 const char* nfft_status_string(nfft_status s);

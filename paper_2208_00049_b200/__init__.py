@@ -26,15 +26,17 @@ NFFT_SYMBOLS = (
     "nfft_default_options", "nfft_plan_create", "nfft_plan_create_ex", "nfft_set_nodes",
     "nfft_precompute", "nfft_forward", "nfft_adjoint", "nfft_plan_destroy", "nfft_status_string",
     "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
-    "nfft_get_launch_count",
+    "nfft_get_launch_count", "nfft_run_stage",
 )
+STAGES = {"precompute": 0, "fwd_deconv": 1, "fwd_fft": 2, "fwd_interp": 3, "adj_spread": 4, "adj_fft": 5,
+          "adj_crop": 6}
 
 STATUS = {
     0: "NFFT_SUCCESS", 1: "NFFT_ERROR_INVALID_VALUE", 2: "NFFT_ERROR_BAD_GEOMETRY",
     3: "NFFT_ERROR_NONFINITE_NODE", 4: "NFFT_ERROR_BAD_TILE", 5: "NFFT_ERROR_NOT_PRECOMPUTED",
     6: "NFFT_ERROR_OUT_OF_MEMORY", 7: "NFFT_ERROR_CUDA", 8: "NFFT_ERROR_CUFFT", 9: "NFFT_ERROR_UNSUPPORTED",
 }
-METHODS = {"auto": 0, "tiled": 1, "direct": 2}
+METHODS = {"auto": 0, "tiled": 1, "direct": 2, "tiled_cas": 3}
 PRECISIONS = {"c64": 0, "c128": 1}
 
 
@@ -82,6 +84,7 @@ def lib():
         "nfft_get_window_tables": [vp, P(ctypes.c_double), P(ctypes.c_double), P(c_int)],
         "nfft_get_stage_times": [vp, c_int, P(ctypes.c_float)],
         "nfft_get_launch_count": [vp, P(i64)],
+        "nfft_run_stage": [vp, c_int, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -223,6 +226,14 @@ class NfftPlan:
         if out is None:
             out = self._empty_like_kind(f, self._grid_shape())
         _check(lib().nfft_adjoint(self._h, _ptr(f), _ptr(out)), "nfft_adjoint")
+        return out
+
+    def run_stage(self, stage, inp=None, out=None):
+        """One stage of Alg. 1/2 on device tensors (nfft_run_stage)."""
+        _check(lib().nfft_run_stage(self._h, STAGES[stage], None if inp is None else _ptr(inp),
+                                    None if out is None else _ptr(out)), f"nfft_run_stage({stage})")
+        if stage == "precompute":
+            self.precomputed = True
         return out
 
     def info(self):

@@ -85,6 +85,18 @@ __device__ __forceinline__ void window_taps(T zeta, const T (&mu)[MAX_M][MAX_Z],
   }
 }
 
+// shared-memory bytes of spread_loc_kernel (host and device agree)
+__host__ __device__ inline size_t loc_smem_bytes(int D, int M, size_t csize, size_t rsize, int region_cells, int S,
+                                                 int nst) {
+  const size_t taps = (size_t)S * D * 2 * M * rsize;
+  size_t b = (size_t)region_cells * csize + taps;
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)S * csize;                        // f values of one batch vector
+  b += (size_t)S * 4 * (2 + D);                  // j, order, loc[D]
+  b += (size_t)(2 * nst + 2) * 4;                // sub-tile offsets and cursors
+  return b;
+}
+
 // ---- block-wide exclusive scan of one int per thread (blockDim = THREADS) ----
 __device__ __forceinline__ int block_exclusive_scan(int x, int* ws, int& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

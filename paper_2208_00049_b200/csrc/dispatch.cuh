@@ -13,6 +13,8 @@ struct KernelSet {
   void (*spread_tiled)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
   void (*interp_direct)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, C*);
   void (*spread_direct)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, C*);
+  void (*spread_loc)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
+  int loc_threads;
 };
 
 template <typename T> KernelSet<T> kernels_d1(int m);
@@ -34,8 +36,13 @@ namespace nfftb {
 template <typename T, int D, int M>
 KernelSet<T> make_set() {
   constexpr int DEG = poly_degree(M, sizeof(T) == 8);
-  return {interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>, interp_direct_kernel<T, D, M, DEG>,
-          spread_direct_kernel<T, D, M, DEG>};
+  KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
+                 interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0};
+  if constexpr (D <= 2) {
+    k.spread_loc = spread_loc_kernel<T, D, M, DEG>;
+    k.loc_threads = LocCfg<T, D, M>::THR;
+  }
+  return k;
 }
 template <typename T, int D>
 KernelSet<T> make_set_m(int m) {

@@ -48,6 +48,8 @@ struct nfft_plan_s {
   int sort_blocks = 1;
   int max_subs = 1;
   int grid_tiled = 1;     // CTAs for the tiled kernels
+  int grid_loc = 0;       // CTAs for the conflict-free spread (0: not used)
+  size_t loc_bytes = 0;
   int grid_direct = 1;
   size_t region_bytes = 0;
   Geom geom{};
@@ -69,6 +71,11 @@ struct nfft_plan_s {
   int* d_subbase = nullptr;  // n_tiles + 1 (last = number of subproblems)
   int4* d_subs = nullptr;
   int* d_err = nullptr;
+  int* d_cnt = nullptr;        // counting sort: [n_tiles][cs_nblk] per-block tile counts
+  int* d_tile_total = nullptr; // n_tiles
+  unsigned* d_ticket = nullptr;
+  bool use_cs = true;
+  int cs_W = 8, cs_E = 2048, cs_nblk = 1;
   void* d_grid = nullptr;    // B * prod Nt complex
   double* d_beta64 = nullptr;
   void* d_betaT = nullptr;
@@ -135,7 +142,8 @@ bool is_device_pointer(const void* p) {
 void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_keys_a, p->d_vals_a, p->d_keys_b, p->d_vals_b, p->d_offsets,
                   p->d_hist, p->d_scan_tmp, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_beta64,
-                  p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes};
+                  p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
+                  p->d_ticket, p->d_perm};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -222,6 +230,23 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
       occ_min = std::min(occ_min, occ);
     }
     p->grid_tiled = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ_min * p->sm_count));
+    p->grid_loc = 0;
+    if (ks.spread_loc && p->opt.method != NFFT_METHOD_TILED_CAS) {
+      int nst = 1;
+      for (int d = 0; d < p->D; ++d) nst *= (int)((p->Q[d] + 2 * p->m - 1) / (2 * p->m));
+      const size_t bytes = loc_smem_bytes(p->D, p->m, p->csize(), p->rsize(), p->geom.region_cells, p->S, nst);
+      int occ = 0;
+      if (bytes <= 227 * 1024 &&
+          cudaFuncSetAttribute((const void*)ks.spread_loc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
+              cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ks.spread_loc, ks.loc_threads, bytes) ==
+              cudaSuccess &&
+          occ >= 1) {
+        p->loc_bytes = bytes;
+        p->grid_loc = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ * p->sm_count));
+      }
+      cudaGetLastError();
+    }
   }
   p->grid_direct = p->sm_count * 8;
   return NFFT_SUCCESS;
@@ -230,9 +255,30 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
 template <typename R>
 nfft_status precompute_impl(nfft_plan p) {
   const int M = (int)p->M;
-  const int nb_bin = (M + THREADS - 1) / THREADS;
+  const int nt = (int)p->n_tiles;
   CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->stream));
   rec(p, 2, 0);
+  if (p->use_cs) {
+    // stable counting sort: 3 kernels (precompute.cuh)
+    const int thr = p->cs_W * 32;
+    cs_count_kernel<R><<<p->cs_nblk, thr, (size_t)nt * 4, p->stream>>>(
+        (const R*)p->d_nodes, p->geom, nt, p->cs_E, p->cs_nblk, p->d_cnt, p->d_err, p->d_ticket);
+    ++p->launches;
+    CKL();
+    cs_scan_kernel<<<(nt + 7) / 8, THREADS, 0, p->stream>>>(p->d_cnt, nt, p->cs_nblk, M, p->d_tile_total,
+                                                           p->d_offsets, p->d_ticket, p->node_begin, p->node_end,
+                                                           p->S, p->d_subbase, p->d_subs);
+    ++p->launches;
+    CKL();
+    cs_scatter_kernel<R><<<p->cs_nblk, thr, (size_t)p->cs_W * nt * 4, p->stream>>>(
+        (const R*)p->d_nodes, p->geom, nt, p->cs_E, p->cs_nblk, p->d_cnt, p->d_offsets, p->d_perm, (R*)p->d_ks);
+    ++p->launches;
+    CKL();
+    rec(p, 2, 1);
+    return NFFT_SUCCESS;
+  }
+  // radix fallback for very many tiles
+  const int nb_bin = (M + THREADS - 1) / THREADS;
   bin_nodes_kernel<R><<<nb_bin, THREADS, 0, p->stream>>>((const R*)p->d_nodes, p->geom, p->d_keys_a, p->d_vals_a,
                                                          p->d_err);
   ++p->launches;
@@ -255,35 +301,119 @@ nfft_status precompute_impl(nfft_plan p) {
     std::swap(ka, kb);
     std::swap(va, vb);
   }
-  p->d_perm = va;
-  const int nt = (int)p->n_tiles;
+  if (va != p->d_perm) CK(cudaMemcpyAsync(p->d_perm, va, (size_t)M * 4, cudaMemcpyDeviceToDevice, p->stream));
   tile_offsets_kernel<<<(M + 1 + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(ka, M, nt, p->d_offsets);
   ++p->launches;
   CKL();
   gather_sorted_kernel<R><<<nb_bin, THREADS, 0, p->stream>>>((const R*)p->d_nodes, p->d_perm, p->geom, (R*)p->d_ks);
   ++p->launches;
   CKL();
-  if (p->tiled) {
-    count_subproblems_kernel<<<(nt + 1 + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
-        p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase);
-    ++p->launches;
-    CKL();
-    nfft_status s = scan_exclusive(p, p->d_subbase, nt + 1, p->d_scan_tmp);
-    if (s != NFFT_SUCCESS) return s;
-    write_subproblems_kernel<<<(nt + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
-        p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase, p->d_subs);
-    ++p->launches;
-    CKL();
-  }
+  count_subproblems_kernel<<<(nt + 1 + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
+      p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase);
+  ++p->launches;
+  CKL();
+  nfft_status s = scan_exclusive(p, p->d_subbase, nt + 1, p->d_scan_tmp);
+  if (s != NFFT_SUCCESS) return s;
+  write_subproblems_kernel<<<(nt + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
+      p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase, p->d_subs);
+  ++p->launches;
+  CKL();
   rec(p, 2, 1);
   return NFFT_SUCCESS;
 }
 
+// ---- stages (each enqueues its kernels on the plan stream; device pointers) ----
+inline int elementwise_blocks(nfft_plan p, long long n) {
+  return (int)std::max<long long>(1, std::min<long long>((n + THREADS - 1) / THREADS, (long long)p->sm_count * 32));
+}
+
+template <typename T>
+nfft_status stage_deconv(nfft_plan p, const typename cplx<T>::type* fhat) {
+  const Geom& g = p->geom;
+  const int nl = g.Nt[g.D - 1];
+  const long long rows = (long long)g.B * (g.grid_cells / nl);
+  dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
+  deconv_pad_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, fhat, (const T*)p->d_betaT,
+                                                        (typename cplx<T>::type*)p->d_grid);
+  ++p->launches;
+  CKL();
+  return NFFT_SUCCESS;
+}
+
+template <typename T>
+nfft_status stage_fft(nfft_plan p, int dir) {
+  cufftResult r;
+  if constexpr (sizeof(T) == 8)
+    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)p->d_grid, (cufftDoubleComplex*)p->d_grid, dir);
+  else
+    r = cufftExecC2C(p->fft, (cufftComplex*)p->d_grid, (cufftComplex*)p->d_grid, dir);
+  return r == CUFFT_SUCCESS ? NFFT_SUCCESS : NFFT_ERROR_CUFFT;
+}
+
+template <typename T>
+nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f) {
+  const KernelSet<T>& ks = kernels_of<T>(p);
+  const WinPoly<T>& wp = poly_of<T>(p);
+  const auto* grid = (const typename cplx<T>::type*)p->d_grid;
+  if (p->tiled) {
+    ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
+        p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
+  } else {
+    ks.interp_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, grid, (const T*)p->d_ks, p->d_perm,
+                                                               p->node_begin, p->node_end, f);
+  }
+  ++p->launches;
+  CKL();
+  return NFFT_SUCCESS;
+}
+
+template <typename T>
+nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
+  const KernelSet<T>& ks = kernels_of<T>(p);
+  const WinPoly<T>& wp = poly_of<T>(p);
+  auto* grid = (typename cplx<T>::type*)p->d_grid;
+  const long long n16 = (long long)(p->geom.grid_cells * p->B * sizeof(typename cplx<T>::type) / 16);
+  zero_kernel<<<elementwise_blocks(p, n16), THREADS, 0, p->stream>>>((float4*)grid, n16);
+  ++p->launches;
+  CKL();
+  rec(p, 1, 1);
+  if (p->tiled && p->grid_loc > 0) {
+    ks.spread_loc<<<p->grid_loc, ks.loc_threads, p->loc_bytes, p->stream>>>(
+        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, p->S, grid);
+  } else if (p->tiled) {
+    ks.spread_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
+        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, grid);
+  } else {
+    ks.spread_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, f, (const T*)p->d_ks, p->d_perm,
+                                                               p->node_begin, p->node_end, grid);
+  }
+  ++p->launches;
+  CKL();
+  return NFFT_SUCCESS;
+}
+
+template <typename T>
+nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y) {
+  const Geom& g = p->geom;
+  const int nl = g.N[g.D - 1];
+  const long long rows = (long long)g.B * (g.ngrid_cells / nl);
+  dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
+  crop_deconv_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, (const typename cplx<T>::type*)p->d_grid,
+                                                         (const T*)p->d_betaT, y);
+  ++p->launches;
+  CKL();
+  return NFFT_SUCCESS;
+}
+
+#define TRY(x)                          \
+  do {                                  \
+    nfft_status s_ = (x);               \
+    if (s_ != NFFT_SUCCESS) return s_;  \
+  } while (0)
+
 template <typename T>
 nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
   using C = typename cplx<T>::type;
-  const KernelSet<T>& ks = kernels_of<T>(p);
-  const WinPoly<T>& wp = poly_of<T>(p);
   const size_t grid_bytes_in = (size_t)p->B * p->geom.ngrid_cells * sizeof(C);
   const size_t node_bytes = (size_t)p->B * p->M * sizeof(C);
   const C* fhat = (const C*)fhat_in;
@@ -299,30 +429,12 @@ nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
     if (!p->d_stage_nodes) CK(cudaMalloc(&p->d_stage_nodes, node_bytes));
     f = (C*)p->d_stage_nodes;
   }
-  C* grid = (C*)p->d_grid;
   rec(p, 0, 0);
-  const long long cells = p->geom.grid_cells * p->B;
-  const int nblk = (int)std::min<long long>((cells + THREADS - 1) / THREADS, (long long)p->sm_count * 16);
-  deconv_pad_kernel<T><<<nblk, THREADS, 0, p->stream>>>(p->geom, fhat, (const T*)p->d_betaT, grid);
-  ++p->launches;
-  CKL();
+  TRY(stage_deconv<T>(p, fhat));
   rec(p, 0, 1);
-  cufftResult r;
-  if constexpr (sizeof(T) == 8)
-    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)grid, (cufftDoubleComplex*)grid, CUFFT_FORWARD);
-  else
-    r = cufftExecC2C(p->fft, (cufftComplex*)grid, (cufftComplex*)grid, CUFFT_FORWARD);
-  if (r != CUFFT_SUCCESS) return NFFT_ERROR_CUFFT;
+  TRY(stage_fft<T>(p, CUFFT_FORWARD));
   rec(p, 0, 2);
-  if (p->tiled) {
-    ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
-        p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
-  } else {
-    ks.interp_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, grid, (const T*)p->d_ks, p->d_perm,
-                                                               p->node_begin, p->node_end, f);
-  }
-  ++p->launches;
-  CKL();
+  TRY(stage_interp<T>(p, f));
   rec(p, 0, 3);
   if (host_out) {
     CK(cudaMemcpyAsync(f_out, f, node_bytes, cudaMemcpyDeviceToHost, p->stream));
@@ -334,8 +446,6 @@ nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
 template <typename T>
 nfft_status adjoint_impl(nfft_plan p, const void* f_in, void* y_out) {
   using C = typename cplx<T>::type;
-  const KernelSet<T>& ks = kernels_of<T>(p);
-  const WinPoly<T>& wp = poly_of<T>(p);
   const size_t grid_bytes_out = (size_t)p->B * p->geom.ngrid_cells * sizeof(C);
   const size_t node_bytes = (size_t)p->B * p->M * sizeof(C);
   const C* f = (const C*)f_in;
@@ -351,42 +461,32 @@ nfft_status adjoint_impl(nfft_plan p, const void* f_in, void* y_out) {
     if (!p->d_stage_grid) CK(cudaMalloc(&p->d_stage_grid, grid_bytes_out));
     y = (C*)p->d_stage_grid;
   }
-  C* grid = (C*)p->d_grid;
   rec(p, 1, 0);
-  const long long n16 = (long long)(p->geom.grid_cells * p->B * sizeof(C) / 16);
-  zero_kernel<<<(int)std::min<long long>((n16 + THREADS - 1) / THREADS, (long long)p->sm_count * 16), THREADS, 0,
-                p->stream>>>((float4*)grid, n16);
-  ++p->launches;
-  CKL();
-  rec(p, 1, 1);
-  if (p->tiled) {
-    ks.spread_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
-        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, grid);
-  } else {
-    ks.spread_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, f, (const T*)p->d_ks, p->d_perm,
-                                                               p->node_begin, p->node_end, grid);
-  }
-  ++p->launches;
-  CKL();
+  TRY(stage_spread<T>(p, f));
   rec(p, 1, 2);
-  cufftResult r;
-  if constexpr (sizeof(T) == 8)
-    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)grid, (cufftDoubleComplex*)grid, CUFFT_INVERSE);
-  else
-    r = cufftExecC2C(p->fft, (cufftComplex*)grid, (cufftComplex*)grid, CUFFT_INVERSE);
-  if (r != CUFFT_SUCCESS) return NFFT_ERROR_CUFFT;
+  TRY(stage_fft<T>(p, CUFFT_INVERSE));
   rec(p, 1, 3);
-  const long long outs = p->geom.ngrid_cells * p->B;
-  const int nblk = (int)std::min<long long>((outs + THREADS - 1) / THREADS, (long long)p->sm_count * 16);
-  crop_deconv_kernel<T><<<nblk, THREADS, 0, p->stream>>>(p->geom, grid, (const T*)p->d_betaT, y);
-  ++p->launches;
-  CKL();
+  TRY(stage_crop<T>(p, y));
   rec(p, 1, 4);
   if (host_out) {
     CK(cudaMemcpyAsync(y_out, y, grid_bytes_out, cudaMemcpyDeviceToHost, p->stream));
     CK(cudaStreamSynchronize(p->stream));
   }
   return NFFT_SUCCESS;
+}
+
+template <typename T>
+nfft_status run_stage_impl(nfft_plan p, int stage, const void* in, void* out) {
+  using C = typename cplx<T>::type;
+  switch (stage) {
+    case NFFT_STAGE_FWD_DECONV: return stage_deconv<T>(p, (const C*)in);
+    case NFFT_STAGE_FWD_FFT: return stage_fft<T>(p, CUFFT_FORWARD);
+    case NFFT_STAGE_FWD_INTERP: return stage_interp<T>(p, (C*)out);
+    case NFFT_STAGE_ADJ_SPREAD: return stage_spread<T>(p, (const C*)in);
+    case NFFT_STAGE_ADJ_FFT: return stage_fft<T>(p, CUFFT_INVERSE);
+    case NFFT_STAGE_ADJ_CROP: return stage_crop<T>(p, (C*)out);
+  }
+  return NFFT_ERROR_INVALID_VALUE;
 }
 
 nfft_status copy_nodes(nfft_plan p, const void* nodes) {
@@ -408,7 +508,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   nfft_default_options(&opt);
   if (opt_in) opt = *opt_in;
   if (opt.batch < 1) return NFFT_ERROR_INVALID_VALUE;
-  if (opt.method < 0 || opt.method > 2) return NFFT_ERROR_INVALID_VALUE;
+  if (opt.method < 0 || opt.method > 3) return NFFT_ERROR_INVALID_VALUE;
   if (!(sigma > 1.0) || !std::isfinite(sigma)) return NFFT_ERROR_BAD_GEOMETRY;
   if (m > MAX_M) return NFFT_ERROR_UNSUPPORTED;
   if (M > (int64_t)0x7fffffff - 1) return NFFT_ERROR_UNSUPPORTED;
@@ -449,7 +549,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   CK(cudaGetDeviceProperties(&prop, dev));
   const size_t smem_max = prop.sharedMemPerBlockOptin;
   bool tiled;
-  if (opt.method == NFFT_METHOD_TILED) {
+  if (opt.method == NFFT_METHOD_TILED || opt.method == NFFT_METHOD_TILED_CAS) {
     if (region_bytes > smem_max) return NFFT_ERROR_BAD_TILE;
     tiled = true;
   } else if (opt.method == NFFT_METHOD_DIRECT) {
@@ -489,6 +589,19 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   p->nbits = 0;
   while (((int64_t)1 << p->nbits) < n_tiles) ++p->nbits;
   p->sort_blocks = (int)((M + SORT_TILE - 1) / SORT_TILE);
+  // counting-sort geometry: W warps per block so the [W][n_tiles] smem table fits 64 KB
+  p->use_cs = false;
+  for (int W = 8; W >= 1; W >>= 1) {
+    const int64_t E = (int64_t)W * 32 * CS_CHUNKS;
+    const int64_t nblk = (M + E - 1) / E;
+    if ((int64_t)W * n_tiles * 4 <= 65536 && n_tiles * nblk <= ((int64_t)1 << 23)) {
+      p->use_cs = true;
+      p->cs_W = W;
+      p->cs_E = (int)E;
+      p->cs_nblk = (int)nblk;
+      break;
+    }
+  }
   p->max_subs = (int)std::min<int64_t>((nend - opt.node_begin + p->S - 1) / p->S + n_tiles, 0x7fffffff);
   if (p->max_subs < 1) p->max_subs = 1;
 
@@ -529,15 +642,38 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   };
   const size_t rs = c128 ? 8 : 4;
   bool ok = alloc(&p->d_nodes, (size_t)M * D * rs) && alloc(&p->d_ks, (size_t)M * D * rs) &&
-            alloc((void**)&p->d_keys_a, M * 4) && alloc((void**)&p->d_vals_a, M * 4) &&
-            alloc((void**)&p->d_keys_b, M * 4) && alloc((void**)&p->d_vals_b, M * 4) &&
-            alloc((void**)&p->d_offsets, (n_tiles + 1) * 4) && alloc((void**)&p->d_hist, 256 * p->sort_blocks * 4) &&
-            alloc((void**)&p->d_scan_tmp, scan_tmp_ints(std::max<int64_t>(256 * p->sort_blocks, n_tiles + 1)) * 4) &&
+            alloc((void**)&p->d_perm, M * 4) && alloc((void**)&p->d_offsets, (n_tiles + 1) * 4) &&
             alloc((void**)&p->d_subbase, (n_tiles + 1) * 4) && alloc((void**)&p->d_subs, (size_t)p->max_subs * 16) &&
             alloc((void**)&p->d_err, 16) && alloc(&p->d_grid, (size_t)cells * p->B * csz) &&
             alloc((void**)&p->d_beta64, boff * 8) && alloc(&p->d_betaT, boff * rs) &&
             alloc((void**)&p->d_poly, (size_t)D * 2 * m * MAX_Z * 8);
+  if (ok && p->use_cs) {
+    ok = alloc((void**)&p->d_cnt, (size_t)n_tiles * p->cs_nblk * 4) && alloc((void**)&p->d_tile_total, n_tiles * 4) &&
+         alloc((void**)&p->d_ticket, 16);
+  } else if (ok) {
+    ok = alloc((void**)&p->d_keys_a, M * 4) && alloc((void**)&p->d_vals_a, M * 4) &&
+         alloc((void**)&p->d_keys_b, M * 4) && alloc((void**)&p->d_vals_b, M * 4) &&
+         alloc((void**)&p->d_hist, 256 * p->sort_blocks * 4) &&
+         alloc((void**)&p->d_scan_tmp, scan_tmp_ints(std::max<int64_t>(256 * p->sort_blocks, n_tiles + 1)) * 4);
+  }
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
+  if (p->use_cs) {
+    const int bytes1 = (int)(n_tiles * 4), bytes3 = (int)(p->cs_W * n_tiles * 4);
+    cudaError_t e = cudaSuccess;
+    if (c128) {
+      e = cudaFuncSetAttribute((const void*)cs_count_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes1);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)cs_scatter_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes3);
+    } else {
+      e = cudaFuncSetAttribute((const void*)cs_count_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes1);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)cs_scatter_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes3);
+    }
+    if (e != cudaSuccess) {
+      last_cuda_error = e;
+      return fail(NFFT_ERROR_CUDA);
+    }
+  }
 
   int n[3];
   for (int d = 0; d < D; ++d) n[d] = (int)Nt[d];
@@ -639,6 +775,22 @@ nfft_status nfft_adjoint(nfft_plan p, const void* f_nodes, void* fhat_grid) {
   DeviceGuard guard(p->device);
   return p->prec == NFFT_COMPLEX128 ? adjoint_impl<double>(p, f_nodes, fhat_grid)
                                     : adjoint_impl<float>(p, f_nodes, fhat_grid);
+}
+
+nfft_status nfft_run_stage(nfft_plan p, int stage, const void* in, void* out) {
+  if (!p || stage < NFFT_STAGE_PRECOMPUTE || stage > NFFT_STAGE_ADJ_CROP) return NFFT_ERROR_INVALID_VALUE;
+  DeviceGuard guard(p->device);
+  if (stage == NFFT_STAGE_PRECOMPUTE) {
+    nfft_status s = p->prec == NFFT_COMPLEX128 ? precompute_impl<double>(p) : precompute_impl<float>(p);
+    if (s == NFFT_SUCCESS) p->precomputed = true;
+    return s;
+  }
+  if (!p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
+  const bool needs_in = stage == NFFT_STAGE_FWD_DECONV || stage == NFFT_STAGE_ADJ_SPREAD;
+  const bool needs_out = stage == NFFT_STAGE_FWD_INTERP || stage == NFFT_STAGE_ADJ_CROP;
+  if ((needs_in && (!in || !is_device_pointer(in))) || (needs_out && (!out || !is_device_pointer(out))))
+    return NFFT_ERROR_INVALID_VALUE;
+  return p->prec == NFFT_COMPLEX128 ? run_stage_impl<double>(p, stage, in, out) : run_stage_impl<float>(p, stage, in, out);
 }
 
 nfft_status nfft_plan_destroy(nfft_plan p) {

@@ -15,7 +15,178 @@ constexpr int SORT_TILE = THREADS * SORT_ITEMS;  // 2048 keys per block
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = THREADS * SCAN_ITEMS;
 
-// ---------------------------------------------------------------- a1 binning
+// Tile key of node j (reading R10); non-finite coordinates -> key 0, bad = true.
+template <typename R>
+__device__ __forceinline__ int node_key(const R* __restrict__ nodes, const Geom& g, int j, R (&k)[MAX_D], bool& bad) {
+  int key = 0;
+  bad = false;
+  for (int d = 0; d < g.D; ++d) {
+    k[d] = nodes[(long long)j * g.D + d];
+    const double kd = (double)k[d];
+    if (!isfinite(kd)) {
+      bad = true;
+      continue;
+    }
+    double frac;
+    const int c = node_cell(kd, g.Ntd[d], g.Nt[d], frac);
+    key = key * g.P[d] + c / g.Q[d];
+  }
+  return bad ? 0 : key;
+}
+
+// ---------------------------------------------------------------- a1+a2: stable counting sort (3 kernels)
+// Block b of the sort owns nodes [b*E, (b+1)*E), E = 32 * W * CS_CHUNKS (W warps).
+// K1 counts tiles per block; K2 scans the [tile][block] counts (warp per tile)
+// and its last CTA scans the tile totals into the tile offsets and writes the
+// subproblem list; K3 re-walks each block in node order and places every node
+// at offsets[tile] + (nodes of that tile in earlier blocks) + (earlier nodes of
+// that tile in this block) — a stable counting sort, so perm is the unique
+// "tile ascending, original index ascending" order (reading R12). K3 also
+// writes the tile-sorted SoA coordinates.
+constexpr int CS_CHUNKS = 8;  // 32-node chunks per warp
+
+template <typename R>
+__global__ void cs_count_kernel(const R* __restrict__ nodes, Geom g, int n_tiles, int E, int nblk,
+                                int* __restrict__ cnt, int* __restrict__ err, unsigned* __restrict__ ticket) {
+  extern __shared__ int hist[];
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) hist[t] = 0;
+  __syncthreads();
+  const int base = blockIdx.x * E;
+  bool any_bad = false;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int j = base + e;
+    if (j >= g.M) break;
+    R k[MAX_D];
+    bool bad;
+    const int key = node_key(nodes, g, j, k, bad);
+    any_bad |= bad;
+    atomicAdd(&hist[key], 1);
+  }
+  if (any_bad) atomicOr(err, 1);
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) cnt[(long long)t * nblk + blockIdx.x] = hist[t];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
+}
+
+__global__ void __launch_bounds__(THREADS) cs_scan_kernel(int* __restrict__ cnt, int n_tiles, int nblk, int M,
+                                                          int* __restrict__ tile_total, int* __restrict__ offsets,
+                                                          unsigned* __restrict__ ticket, int nb, int ne, int S,
+                                                          int* __restrict__ subbase, int4* __restrict__ subs) {
+  __shared__ int ws[32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (t < n_tiles) {
+    int* row = cnt + (long long)t * nblk;
+    const int per = (nblk + 31) / 32;
+    const int lo = lane * per, hi = min(nblk, lo + per);
+    int s = 0;
+    for (int i = lo; i < hi; ++i) s += row[i];
+    int inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int run = inc - s;
+    for (int i = lo; i < hi; ++i) {
+      const int c = row[i];
+      row[i] = run;
+      run += c;
+    }
+    if (lane == 31) tile_total[t] = inc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // last CTA: tile offsets = exclusive scan of the tile totals
+  {
+    const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per, hi = min(n_tiles, lo + per);
+    int s = 0;
+    for (int i = lo; i < hi; ++i) s += __ldcg(tile_total + i);
+    int total;
+    int run = block_exclusive_scan(s, ws, total);
+    for (int i = lo; i < hi; ++i) {
+      offsets[i] = run;
+      run += __ldcg(tile_total + i);
+    }
+    if (threadIdx.x == 0) offsets[n_tiles] = M;
+  }
+  __syncthreads();
+  // subproblems: shard [nb, ne) of each tile cut into chunks of <= S nodes
+  {
+    const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per, hi = min(n_tiles, lo + per);
+    int s = 0;
+    for (int i = lo; i < hi; ++i) {
+      const int a = max(offsets[i], nb), b = min(offsets[i + 1], ne);
+      s += (max(0, b - a) + S - 1) / S;
+    }
+    int total;
+    int q = block_exclusive_scan(s, ws, total);
+    for (int i = lo; i < hi; ++i) {
+      subbase[i] = q;
+      const int a = max(offsets[i], nb), b = min(offsets[i + 1], ne);
+      for (int st = a; st < b; st += S) subs[q++] = make_int4(i, st, min(S, b - st), 0);
+    }
+    if (threadIdx.x == 0) subbase[n_tiles] = total;
+  }
+}
+
+template <typename R>
+__global__ void cs_scatter_kernel(const R* __restrict__ nodes, Geom g, int n_tiles, int E, int nblk,
+                                  const int* __restrict__ cnt, const int* __restrict__ offsets,
+                                  int* __restrict__ perm, R* __restrict__ ks) {
+  extern __shared__ int wb[];  // [W][n_tiles]
+  const int W = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < W * n_tiles; i += blockDim.x) wb[i] = 0;
+  __syncthreads();
+  const int base = blockIdx.x * E + warp * 32 * CS_CHUNKS;
+  int keys[CS_CHUNKS];
+  R kc[CS_CHUNKS][MAX_D];
+  int* mine = wb + warp * n_tiles;
+#pragma unroll
+  for (int c = 0; c < CS_CHUNKS; ++c) {
+    const int j = base + c * 32 + lane;
+    bool bad;
+    keys[c] = j < g.M ? node_key(nodes, g, j, kc[c], bad) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, keys[c]);
+    if (keys[c] >= 0 && lane == __ffs(peers) - 1) mine[keys[c]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    int run = offsets[t] + cnt[(long long)t * nblk + blockIdx.x];
+    for (int w = 0; w < W; ++w) {
+      const int c = wb[w * n_tiles + t];
+      wb[w * n_tiles + t] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int c = 0; c < CS_CHUNKS; ++c) {
+    const int key = keys[c];
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    int pos = 0;
+    if (key >= 0) pos = mine[key] + __popc(peers & lt);
+    __syncwarp();
+    if (key >= 0 && lane == __ffs(peers) - 1) mine[key] += __popc(peers);
+    __syncwarp();
+    if (key >= 0) {
+      perm[pos] = base + c * 32 + lane;
+      for (int d = 0; d < g.D; ++d) ks[(long long)d * g.M + pos] = kc[c][d];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- a1 binning (radix fallback path)
 // key_j = C-order linear tile id of the cell node j starts from; vals_j = j.
 template <typename R>
 __global__ void __launch_bounds__(THREADS) bin_nodes_kernel(const R* __restrict__ nodes, Geom g,

@@ -286,6 +286,181 @@ __global__ void __launch_bounds__(THREADS) spread_tiled_kernel(Geom g, WinPoly<T
   }
 }
 
+// ------------------------------------------------------------ adjoint, tiled, conflict-free
+// "Lanes own cells" spreading (spread): no shared-memory
+// atomics (fp32/fp64 shared atomics are CAS loops on sm_100a). The subproblem's
+// nodes are bucketed by 2m-wide sub-tiles of the tile; sub-tiles are coloured
+// by the parity of their index in every dimension, so the footprints of nodes
+// in two different sub-tiles of one colour never overlap. Colours run one after
+// another (barrier between); within a colour each worker (G lanes) walks the
+// nodes of its sub-tiles in order and adds one node's (2m)^D footprint per
+// G-cell step with plain loads/stores, each lane owning distinct cells. Taps
+// are computed once per node (even/odd polynomial, registers) and kept in
+// shared memory for all batch vectors. The tile region (+ halo) is flushed to
+// the grid with vector reductions, the GPU form of Alg. 4's locked merge.
+__host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
+
+template <typename T, int D, int M>
+struct LocCfg {
+  static constexpr int TAPS = 2 * M;
+  static constexpr int F = ipow_c(TAPS, D);  // footprint cells
+  static constexpr int G = F < 32 ? F : 32;  // lanes per node
+  static constexpr int WPW = 32 / G;         // workers per warp
+  static constexpr int STEPS = (F + G - 1) / G;
+  static constexpr int THR = D == 1 ? 256 : 128;
+};
+
+template <typename T, int D, int M, int DEG>
+__global__ void __launch_bounds__(LocCfg<T, D, M>::THR) spread_loc_kernel(
+    Geom g, WinPoly<T> wp, const typename cplx<T>::type* __restrict__ f, const T* __restrict__ ks,
+    const int* __restrict__ perm, const int4* __restrict__ subs, const int* __restrict__ nsub_ptr, int S,
+    typename cplx<T>::type* __restrict__ grid) {
+  using C = typename cplx<T>::type;
+  using L = LocCfg<T, D, M>;
+  constexpr int TAPS = L::TAPS, F = L::F, G = L::G, STEPS = L::STEPS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int NS[MAX_D], nst = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    NS[d] = (g.Q[d] + TAPS - 1) / TAPS;
+    nst *= NS[d];
+  }
+  C* acc = reinterpret_cast<C*>(smem_raw);
+  T* tap = reinterpret_cast<T*>(acc + g.region_cells);  // [S][D][TAPS]
+  size_t off = ((size_t)g.region_cells * sizeof(C) + (size_t)S * D * TAPS * sizeof(T) + 15) & ~(size_t)15;
+  C* fv = reinterpret_cast<C*>(smem_raw + off);
+  int* jv = reinterpret_cast<int*>(fv + S);
+  int* order = jv + S;
+  int* lv = order + S;       // [D][S]
+  int* stoff = lv + D * S;   // [nst + 1]
+  int* stcur = stoff + nst + 1;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lg = lane % G;
+  const bool worker_lane = lane < L::WPW * G;  // e.g. m = 3 in 1D: 5 groups of 6 lanes, 2 idle lanes
+  const int worker = worker_lane ? warp * L::WPW + lane / G : 1 << 30;
+  const int nworkers = (blockDim.x >> 5) * L::WPW;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane / G * G));
+  int strides[MAX_D];
+  strides[D - 1] = 1;
+#pragma unroll
+  for (int d = D - 2; d >= 0; --d) strides[d] = strides[d + 1] * g.L[d + 1];
+
+  const int nsub = *nsub_ptr;
+  for (int sidx = blockIdx.x; sidx < nsub; sidx += gridDim.x) {
+    const int4 sp = subs[sidx];
+    const TileCoords tc = tile_coords<D, M>(g, sp.x);
+    for (int i = threadIdx.x; i <= nst; i += blockDim.x) stoff[i] = 0;
+    __syncthreads();
+    // 1. node setup: taps into shared memory, sub-tile histogram
+    for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
+      const int i = sp.y + t;
+      int loc[D];
+      T w[D][TAPS];
+      const bool ok = node_setup<T, D, M, DEG>(g, wp, ks, i, tc, loc, w);
+      jv[t] = ok ? perm[i] : -1;
+      int st = 0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        lv[d * S + t] = loc[d];
+        st = st * NS[d] + (ok ? loc[d] / TAPS : 0);
+#pragma unroll
+        for (int l = 0; l < TAPS; ++l) tap[(t * D + d) * TAPS + l] = w[d][l];
+      }
+      order[t] = st;  // temporarily the sub-tile id
+      if (ok) atomicAdd(&stoff[st + 1], 1);
+    }
+    __syncthreads();
+    // 2. exclusive offsets of the sub-tile buckets (nst is small)
+    if (threadIdx.x == 0) {
+      for (int q = 1; q <= nst; ++q) stoff[q] += stoff[q - 1];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nst; q += blockDim.x) stcur[q] = stoff[q];
+    __syncthreads();
+    int myslot[8];
+    int nmine = 0;
+    for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
+      if (jv[t] >= 0) myslot[nmine] = atomicAdd(&stcur[order[t]], 1);
+      ++nmine;
+    }
+    __syncthreads();
+    nmine = 0;
+    for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
+      if (jv[t] >= 0) order[myslot[nmine]] = t;
+      ++nmine;
+    }
+    __syncthreads();
+    // 3. per batch vector: stage f, zero the tile, coloured conflict-free accumulation, flush
+    for (int b = 0; b < g.B; ++b) {
+      for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
+        const int j = jv[t];
+        if (j >= 0) fv[t] = f[(long long)b * g.M + j];
+      }
+      for (int r = threadIdx.x; r < g.region_cells; r += blockDim.x) {
+        acc[r].x = (T)0;
+        acc[r].y = (T)0;
+      }
+      __syncthreads();
+      for (int color = 0; color < (1 << D); ++color) {
+        int cnt[MAX_D], nu = 1;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int par = (color >> (D - 1 - d)) & 1;
+          cnt[d] = (NS[d] - par + 1) / 2;
+          nu *= cnt[d];
+        }
+        for (int u = worker; u < nu; u += nworkers) {
+          int st = 0, rem = u, ud[MAX_D];
+#pragma unroll
+          for (int d = D - 1; d >= 0; --d) {
+            ud[d] = rem % cnt[d];
+            rem /= cnt[d];
+          }
+#pragma unroll
+          for (int d = 0; d < D; ++d) st = st * NS[d] + 2 * ud[d] + ((color >> (D - 1 - d)) & 1);
+          const int q1 = stoff[st + 1];
+          for (int q = stoff[st]; q < q1; ++q) {
+            const int t = order[q];
+            const C v = fv[t];
+            int base = 0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) base += lv[d * S + t] * strides[d];
+            const T* tp = tap + t * D * TAPS;
+#pragma unroll
+            for (int s2 = 0; s2 < STEPS; ++s2) {
+              const int c = lg + G * s2;
+              if (F % G == 0 || c < F) {
+                T w = (T)1;
+                int a = base, rc = c;
+#pragma unroll
+                for (int d = D - 1; d >= 0; --d) {
+                  const int l = rc % TAPS;
+                  rc /= TAPS;
+                  w *= tp[d * TAPS + l];
+                  a += l * strides[d];
+                }
+                C x = acc[a];
+                x.x = fma(w, v.x, x.x);
+                x.y = fma(w, v.y, x.y);
+                acc[a] = x;
+              }
+            }
+            __syncwarp(gmask);
+          }
+        }
+        __syncthreads();
+      }
+      C* dst = grid + (long long)b * g.grid_cells;
+      for_region<D>(g, tc, [&](int r, long long o) {
+        const C x = acc[r];
+        if (x.x != (T)0 || x.y != (T)0) red_add<T>(dst + o, x);
+      });
+      __syncthreads();
+    }
+  }
+}
+
 // ------------------------------------------------------------ direct (unblocked)
 template <typename T, int D, int M, int DEG>
 __global__ void __launch_bounds__(THREADS) interp_direct_kernel(Geom g, WinPoly<T> wp,

@@ -146,21 +146,21 @@ def test_window_tables_against_oracle_window(m, precision):
 # ------------------------------------------------------------------ forward / adjoint parity
 
 @pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
-@pytest.mark.parametrize("method", ["tiled", "direct"])
+@pytest.mark.parametrize("method", ["tiled", "tiled_cas", "direct"])
 def test_config1_all_m(m, method):
     """BASELINE configs[0] (1D N=256, M=256) at every compiled m; ragged tiles."""
     w = workloads.make("cfg1_1d_256", seed=0, m=m)
     _check(w, method=method, tile=(96,))
 
 
-@pytest.mark.parametrize("method", ["tiled", "direct"])
+@pytest.mark.parametrize("method", ["tiled", "tiled_cas", "direct"])
 @pytest.mark.parametrize("m", [3, 4, 8])
 def test_2d_small_ragged_tiles(method, m):
     w = workloads.make("cfg3_2d_512", seed=1, N=(48, 40), M=3000, m=m)
     _check(w, method=method, tile=(20, 14))
 
 
-@pytest.mark.parametrize("method", ["tiled", "direct"])
+@pytest.mark.parametrize("method", ["tiled", "tiled_cas", "direct"])
 @pytest.mark.parametrize("m", [2, 4, 5])
 def test_3d_small_ragged_tiles(method, m):
     w = workloads.make("cfg4_3d_64", seed=2, N=(16, 12, 10), M=2000, m=m)

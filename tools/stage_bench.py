@@ -1,13 +1,24 @@
-"""Per-stage timing sweep (diagnostic): python tools/stage_bench.py [config] [m] [method] [tile]"""
-import os, sys, statistics, json
+"""Per-stage timing sweep (diagnostic; bench.py is the reference harness).
+
+    python tools/stage_bench.py [config m method tile]
+
+Each stage is captured in its own CUDA graph and timed with events on the
+plan stream after an L2 flush; prints the median microseconds per stage.
+"""
+import json
+import os
+import statistics
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+
 import paper_2208_00049_b200 as pkg
 from paper_2208_00049_b200 import workloads
 
 
-def run(config, m, method="auto", tile=None, steps=20, flush=True):
-    w = workloads.make(config, seed=0, m=m)
+def run(config, m, method="auto", tile=None, steps=20, flush=True, **over):
+    w = workloads.make(config, seed=0, m=m, **over)
     dev = torch.device("cuda", 0)
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
@@ -15,21 +26,43 @@ def run(config, m, method="auto", tile=None, steps=20, flush=True):
         fhat = torch.from_numpy(w["fhat"]).to(dev)
         f = torch.from_numpy(w["f"]).to(dev)
         p = pkg.NfftPlan(nodes, w["N"], m=m, sigma=w["sigma"], precision=w["precision"], batch=w["batch"],
-                         tile=tile, stream=st.cuda_stream, method=method, timing=True, check_nodes=False)
+                         tile=tile, stream=st.cuda_stream, method=method, check_nodes=False)
         fo = torch.empty((w["batch"], w["M"]), dtype=p.tdtype_c, device=dev)
         yo = torch.empty((w["batch"],) + tuple(w["N"]), dtype=p.tdtype_c, device=dev)
         buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        rbuf = torch.ones(64 << 20, dtype=torch.float32, device=dev)
+        sink = torch.empty((), dtype=torch.float32, device=dev)
+    stages = [("pre", lambda: p.run_stage("precompute")), ("deconv", lambda: p.run_stage("fwd_deconv", fhat)),
+              ("fftF", lambda: p.run_stage("fwd_fft")), ("interp", lambda: p.run_stage("fwd_interp", None, fo)),
+              ("spread", lambda: p.run_stage("adj_spread", f)), ("fftA", lambda: p.run_stage("adj_fft")),
+              ("crop", lambda: p.run_stage("adj_crop", None, yo))]
+    with torch.cuda.stream(st):
+        for _, fn in stages:
+            fn()
+    st.synchronize()
+    graphs = []
+    for name, fn in stages:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            fn()
+        graphs.append((name, g))
+    st.synchronize()
     acc = {}
     for s in range(steps + 3):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(graphs) + 1)]
         with torch.cuda.stream(st):
             if flush:
                 buf.zero_()
-            p.precompute(); p.forward(fhat, out=fo); p.adjoint(f, out=yo)
-        tf = p.stage_times("forward"); ta = p.stage_times("adjoint")
+                sink.copy_(rbuf.sum())
+            for k, (_, g) in enumerate(graphs):
+                ev[k].record(st)
+                g.replay()
+            ev[-1].record(st)
+        st.synchronize()
         if s >= 3:
-            for k, v in (("pre", tf["precompute"]), ("deconv", tf["deconv"]), ("fftF", tf["fft"]), ("interp", tf["resample"]),
-                         ("zero", ta["zero"]), ("spread", ta["resample"]), ("fftA", ta["fft"]), ("crop", ta["deconv"])):
-                acc.setdefault(k, []).append(v * 1000)
+            for k, (name, _) in enumerate(graphs):
+                acc.setdefault(name, []).append(ev[k].elapsed_time(ev[k + 1]) * 1000)
+            acc.setdefault("STEP", []).append(ev[0].elapsed_time(ev[-1]) * 1000)
     info = p.info()
     p.close()
     return {k: round(statistics.median(v), 1) for k, v in acc.items()}, info
@@ -49,5 +82,5 @@ if __name__ == "__main__":
         try:
             r, info = run(cfg, m, meth, tile)
             print(json.dumps({"cfg": cfg, "m": m, "method": meth, "tile": info["tile"], "us": r}), flush=True)
-        except Exception as e:
+        except Exception as e:  # keep sweeping
             print(json.dumps({"cfg": cfg, "m": m, "method": meth, "error": str(e)}), flush=True)
