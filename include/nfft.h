@@ -66,9 +66,13 @@ typedef enum {
 /* Resampling kernels. */
 typedef enum {
   NFFT_METHOD_AUTO = 0,   /* tiled when the tile+halo fits shared memory */
-  NFFT_METHOD_TILED = 1,  /* Alg. 3/4: grid tile + m-halo staged in shared memory */
+  NFFT_METHOD_TILED = 1,  /* Alg. 3/4: grid tile + m-halo staged in shared memory;
+                             adjoint as a per-cell gather over cell-sorted nodes (D <= 2) */
   NFFT_METHOD_DIRECT = 2, /* unblocked resampling straight from L2/HBM */
-  NFFT_METHOD_TILED_CAS = 3 /* tiled, adjoint with shared-memory atomics (reference variant) */
+  NFFT_METHOD_TILED_CAS = 3, /* tiled; adjoint accumulates with shared-memory atomics (reference variant) */
+  NFFT_METHOD_TILED_LOC = 4, /* tiled; adjoint lanes-own-cells + global reduction flush (D <= 2) */
+  NFFT_METHOD_TILED_OWN = 5, /* tiled; adjoint owner-computes, no atomics, no zero pass (D <= 2) */
+  NFFT_METHOD_TILED_SORTED = 6 /* tiled; adjoint thread-per-node over cell-sorted warp chunks */
 } nfft_method;
 
 typedef struct {

@@ -97,6 +97,27 @@ __host__ __device__ inline size_t loc_smem_bytes(int D, int M, size_t csize, siz
   return b;
 }
 
+__host__ __device__ inline size_t own_smem_bytes(int D, int M, size_t csize, size_t rsize, int tile_cells, int thr,
+                                                 int nst_ext) {
+  size_t b = (size_t)tile_cells * csize;                   // accumulator
+  b += (size_t)thr * D * 2 * M * rsize;                    // taps of one chunk
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)thr * csize;                                // f values of the chunk
+  b += (size_t)thr * 4 * (1 + 1 + D);                      // node j, order, footprint start per dim
+  b += (size_t)2048 * 4;                                   // relevant-node list (sorted positions)
+  b += (size_t)(2 * nst_ext + 4) * 4;                      // bucket offsets, cursors, counters
+  return b;
+}
+
+__host__ __device__ inline size_t gather_smem_bytes(int D, int M, size_t csize, size_t rsize, int tile_cells, int S) {
+  size_t b = (size_t)S * D * 2 * M * rsize;  // taps per sorted slot
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)S * csize;                    // f of the current batch vector
+  b += (size_t)S * 4 * (D + 1);              // local cell per dim, node j
+  b += (size_t)2 * (tile_cells + 1) * 4;     // cell offsets, cursors
+  return b;
+}
+
 // ---- block-wide exclusive scan of one int per thread (blockDim = THREADS) ----
 __device__ __forceinline__ int block_exclusive_scan(int x, int* ws, int& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

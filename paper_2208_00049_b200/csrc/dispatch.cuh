@@ -15,6 +15,10 @@ struct KernelSet {
   void (*spread_direct)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, C*);
   void (*spread_loc)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
   int loc_threads;
+  void (*spread_own)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
+  int own_threads;
+  void (*spread_sorted)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
+  void (*spread_gather)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
 };
 
 template <typename T> KernelSet<T> kernels_d1(int m);
@@ -37,10 +41,14 @@ template <typename T, int D, int M>
 KernelSet<T> make_set() {
   constexpr int DEG = poly_degree(M, sizeof(T) == 8);
   KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
-                 interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0};
+                 interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
+                 spread_sorted_kernel<T, D, M, DEG>, nullptr};
   if constexpr (D <= 2) {
     k.spread_loc = spread_loc_kernel<T, D, M, DEG>;
     k.loc_threads = LocCfg<T, D, M>::THR;
+    k.spread_own = spread_own_kernel<T, D, M, DEG>;
+    k.own_threads = OwnCfg<T, D, M>::THR;
+    k.spread_gather = spread_gather_kernel<T, D, M, DEG>;
   }
   return k;
 }

@@ -50,6 +50,12 @@ struct nfft_plan_s {
   int grid_tiled = 1;     // CTAs for the tiled kernels
   int grid_loc = 0;       // CTAs for the conflict-free spread (0: not used)
   size_t loc_bytes = 0;
+  int grid_own = 0;       // CTAs for the owner-computes spread (0: not used)
+  size_t own_bytes = 0;
+  int grid_sorted = 0;    // CTAs for the cell-sorted warp-chunk spread (0: not used)
+  size_t sorted_bytes = 0;
+  int grid_gather = 0;    // CTAs for the cell-gather spread (0: not used)
+  size_t gather_bytes = 0;
   int grid_direct = 1;
   size_t region_bytes = 0;
   Geom geom{};
@@ -230,8 +236,42 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
       occ_min = std::min(occ_min, occ);
     }
     p->grid_tiled = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ_min * p->sm_count));
+    p->grid_gather = 0;
+    if (ks.spread_gather && p->opt.method <= NFFT_METHOD_TILED) {
+      int tile_cells = 1;
+      for (int d = 0; d < p->D; ++d) tile_cells *= (int)p->Q[d];
+      const size_t bytes = gather_smem_bytes(p->D, p->m, p->csize(), p->rsize(), tile_cells, p->S);
+      int occ = 0;
+      if (bytes <= 227 * 1024 &&
+          cudaFuncSetAttribute((const void*)ks.spread_gather, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)bytes) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ks.spread_gather, THREADS, bytes) ==
+              cudaSuccess &&
+          occ >= 1) {
+        p->gather_bytes = bytes;
+        p->grid_gather = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ * p->sm_count));
+      }
+      cudaGetLastError();
+    }
+    p->grid_sorted = 0;
+    if (p->opt.method == NFFT_METHOD_TILED_SORTED || (p->opt.method <= NFFT_METHOD_TILED && p->D == 3)) {
+      int tile_cells = 1;
+      for (int d = 0; d < p->D; ++d) tile_cells *= (int)p->Q[d];
+      const size_t bytes = p->region_bytes + (size_t)(tile_cells + 1 + THREADS + 17) * 4;
+      int occ = 0;
+      if (bytes <= 227 * 1024 &&
+          cudaFuncSetAttribute((const void*)ks.spread_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)bytes) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ks.spread_sorted, THREADS, bytes) ==
+              cudaSuccess &&
+          occ >= 1) {
+        p->sorted_bytes = bytes;
+        p->grid_sorted = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ * p->sm_count));
+      }
+      cudaGetLastError();
+    }
     p->grid_loc = 0;
-    if (ks.spread_loc && p->opt.method != NFFT_METHOD_TILED_CAS) {
+    if (ks.spread_loc && p->opt.method == NFFT_METHOD_TILED_LOC) {
       int nst = 1;
       for (int d = 0; d < p->D; ++d) nst *= (int)((p->Q[d] + 2 * p->m - 1) / (2 * p->m));
       const size_t bytes = loc_smem_bytes(p->D, p->m, p->csize(), p->rsize(), p->geom.region_cells, p->S, nst);
@@ -244,6 +284,28 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
           occ >= 1) {
         p->loc_bytes = bytes;
         p->grid_loc = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ * p->sm_count));
+      }
+      cudaGetLastError();
+    }
+    p->grid_own = 0;
+    bool own_ok = ks.spread_own != nullptr && p->opt.method == NFFT_METHOD_TILED_OWN;
+    int tile_cells = 1, nstx = 1;
+    for (int d = 0; d < p->D && own_ok; ++d) {
+      own_ok = p->P[d] >= 3 && p->Nt[d] % p->Q[d] == 0 && p->Q[d] >= 2 * p->m;
+      tile_cells *= (int)p->Q[d];
+      nstx *= (int)((p->Q[d] + 2 * p->m - 1) / (2 * p->m) + 2);
+    }
+    if (own_ok) {
+      const size_t bytes = own_smem_bytes(p->D, p->m, p->csize(), p->rsize(), tile_cells, ks.own_threads, nstx);
+      int occ = 0;
+      if (bytes <= 227 * 1024 &&
+          cudaFuncSetAttribute((const void*)ks.spread_own, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
+              cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ks.spread_own, ks.own_threads, bytes) ==
+              cudaSuccess &&
+          occ >= 1) {
+        p->own_bytes = bytes;
+        p->grid_own = (int)std::max<int64_t>(1, std::min<int64_t>(p->n_tiles, (int64_t)occ * p->sm_count));
       }
       cudaGetLastError();
     }
@@ -372,12 +434,27 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   auto* grid = (typename cplx<T>::type*)p->d_grid;
+  if (p->tiled && p->grid_own > 0) {
+    // owner-computes: every grid cell written exactly once, no zero pass
+    rec(p, 1, 1);
+    ks.spread_own<<<p->grid_own, ks.own_threads, p->own_bytes, p->stream>>>(
+        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, grid);
+    ++p->launches;
+    CKL();
+    return NFFT_SUCCESS;
+  }
   const long long n16 = (long long)(p->geom.grid_cells * p->B * sizeof(typename cplx<T>::type) / 16);
   zero_kernel<<<elementwise_blocks(p, n16), THREADS, 0, p->stream>>>((float4*)grid, n16);
   ++p->launches;
   CKL();
   rec(p, 1, 1);
-  if (p->tiled && p->grid_loc > 0) {
+  if (p->tiled && p->grid_gather > 0) {
+    ks.spread_gather<<<p->grid_gather, THREADS, p->gather_bytes, p->stream>>>(
+        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, p->S, grid);
+  } else if (p->tiled && p->grid_loc == 0 && p->grid_sorted > 0) {
+    ks.spread_sorted<<<p->grid_sorted, THREADS, p->sorted_bytes, p->stream>>>(
+        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, grid);
+  } else if (p->tiled && p->grid_loc > 0) {
     ks.spread_loc<<<p->grid_loc, ks.loc_threads, p->loc_bytes, p->stream>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, p->S, grid);
   } else if (p->tiled) {
@@ -508,7 +585,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   nfft_default_options(&opt);
   if (opt_in) opt = *opt_in;
   if (opt.batch < 1) return NFFT_ERROR_INVALID_VALUE;
-  if (opt.method < 0 || opt.method > 3) return NFFT_ERROR_INVALID_VALUE;
+  if (opt.method < 0 || opt.method > 6) return NFFT_ERROR_INVALID_VALUE;
   if (!(sigma > 1.0) || !std::isfinite(sigma)) return NFFT_ERROR_BAD_GEOMETRY;
   if (m > MAX_M) return NFFT_ERROR_UNSUPPORTED;
   if (M > (int64_t)0x7fffffff - 1) return NFFT_ERROR_UNSUPPORTED;
@@ -538,8 +615,18 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     Q[d] = q;
     P[d] = (Nt[d] + q - 1) / q;
   }
+  // tile region per dimension: Q + 2m - 1 cells (block index set); the contiguous last
+  // dimension is padded for the bank-rotated interp loop (C128: TP - 1 readable cells, pitch % 8 == 0)
+  int64_t Lreg[3] = {1, 1, 1};
   size_t region_cells = 1;
-  for (int d = 0; d < D; ++d) region_cells *= (size_t)(Q[d] + 2 * m - 1);
+  for (int d = 0; d < D; ++d) {
+    Lreg[d] = Q[d] + 2 * m - 1;
+    if (d == D - 1 && precision == NFFT_COMPLEX128) {
+      const int64_t tp = 2 * m <= 8 ? 8 : 16;
+      Lreg[d] = ((Q[d] + tp - 1) + 7) / 8 * 8;
+    }
+    region_cells *= (size_t)Lreg[d];
+  }
   const size_t region_bytes = region_cells * csz;
 
   DeviceGuard guard(opt.device);
@@ -549,7 +636,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   CK(cudaGetDeviceProperties(&prop, dev));
   const size_t smem_max = prop.sharedMemPerBlockOptin;
   bool tiled;
-  if (opt.method == NFFT_METHOD_TILED || opt.method == NFFT_METHOD_TILED_CAS) {
+  if (opt.method != NFFT_METHOD_AUTO && opt.method != NFFT_METHOD_DIRECT) {
     if (region_bytes > smem_max) return NFFT_ERROR_BAD_TILE;
     tiled = true;
   } else if (opt.method == NFFT_METHOD_DIRECT) {
@@ -618,7 +705,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     g.N[d] = act ? (int)N[d] : 1;
     g.Q[d] = act ? (int)Q[d] : 1;
     g.P[d] = act ? (int)P[d] : 1;
-    g.L[d] = act ? (int)(Q[d] + 2 * m - 1) : 1;
+    g.L[d] = act ? (int)Lreg[d] : 1;
     g.Ntd[d] = act ? (double)Nt[d] : 1.0;
     g.beta_off[d] = boff;
     if (act) boff += (int)N[d];

@@ -102,37 +102,82 @@ __device__ __forceinline__ void for_region(const Geom& g, const TileCoords& tc, 
   }
 }
 
+// Padded tap count for the bank-rotated inner loop (C128: 16-byte cells, 8 per
+// 128-byte shared-memory row of banks).
+template <typename T, int M>
+struct RotCfg {
+  static constexpr bool ON = sizeof(T) == 8;
+  static constexpr int TP = ON ? ((2 * M <= 8) ? 8 : 16) : 2 * M;
+};
+
+// w_out[k] = w[(k + rot) mod TP] (zero-padded beyond 2m) with a log2(TP)-stage
+// select network: no dynamic register indexing.
+template <typename T, int M, int TP>
+__device__ __forceinline__ void rotate_taps(const T (&w)[2 * M], int rot, T (&out)[TP]) {
+#pragma unroll
+  for (int k = 0; k < TP; ++k) out[k] = k < 2 * M ? w[k] : (T)0;
+#pragma unroll
+  for (int b = 1; b < TP; b <<= 1) {
+    const bool on = (rot & b) != 0;
+    T tmp[TP];
+#pragma unroll
+    for (int k = 0; k < TP; ++k) tmp[k] = out[(k + b) % TP];
+#pragma unroll
+    for (int k = 0; k < TP; ++k) out[k] = on ? tmp[k] : out[k];
+  }
+}
+
+// Contiguous sum over the last dimension: sum_l w[l] row[l]. With RotCfg::ON
+// lane L reads element (k + rot) mod TP at step k, rot = (L - loc) mod TP, so
+// the 8 lanes of each LDS.128 phase touch 8 distinct bank quads whatever the
+// node positions (requires the region row pitch to be a multiple of 8 cells
+// and TP - 2m readable padding cells, both provided by the plan geometry).
+template <typename T, int M>
+__device__ __forceinline__ typename cplx<T>::type row_sum(const typename cplx<T>::type* row, const T (&wr)[RotCfg<T, M>::TP],
+                                                          const T (&w)[2 * M], int rot) {
+  using C = typename cplx<T>::type;
+  C s;
+  s.x = (T)0;
+  s.y = (T)0;
+  if constexpr (RotCfg<T, M>::ON) {
+    constexpr int TP = RotCfg<T, M>::TP;
+#pragma unroll
+    for (int k = 0; k < TP; ++k) {
+      const C v = row[(k + rot) & (TP - 1)];
+      s.x = fma(wr[k], v.x, s.x);
+      s.y = fma(wr[k], v.y, s.y);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < 2 * M; ++l) {
+      const C v = row[l];
+      s.x = fma(w[l], v.x, s.x);
+      s.y = fma(w[l], v.y, s.y);
+    }
+  }
+  return s;
+}
+
 // (2m)^D tensor-product sum over a region held in shared memory (eq.
 // InnerTensorStructure): innermost dimension contiguous.
 template <typename T, int D, int M>
 __device__ __forceinline__ typename cplx<T>::type gather_tile(const Geom& g, const typename cplx<T>::type* tile,
                                                               const int (&loc)[D], const T (&w)[D][2 * M]) {
   using C = typename cplx<T>::type;
+  constexpr int TP = RotCfg<T, M>::TP;
+  T wr[TP];
+  const int rot = ((int)(threadIdx.x & 31) - loc[D - 1]) & (TP - 1);
+  if constexpr (RotCfg<T, M>::ON) rotate_taps<T, M, TP>(w[D - 1], rot, wr);
   C acc;
   acc.x = (T)0;
   acc.y = (T)0;
   if (D == 1) {
-    const C* row = tile + loc[0];
-#pragma unroll
-    for (int l = 0; l < 2 * M; ++l) {
-      const C v = row[l];
-      acc.x = fma(w[0][l], v.x, acc.x);
-      acc.y = fma(w[0][l], v.y, acc.y);
-    }
+    acc = row_sum<T, M>(tile + loc[0], wr, w[D - 1], rot);
   } else if (D == 2) {
     const int L1 = g.L[1];
 #pragma unroll
     for (int l0 = 0; l0 < 2 * M; ++l0) {
-      const C* row = tile + (loc[0] + l0) * L1 + loc[1];
-      C s;
-      s.x = (T)0;
-      s.y = (T)0;
-#pragma unroll
-      for (int l1 = 0; l1 < 2 * M; ++l1) {
-        const C v = row[l1];
-        s.x = fma(w[1][l1], v.x, s.x);
-        s.y = fma(w[1][l1], v.y, s.y);
-      }
+      const C s = row_sum<T, M>(tile + (loc[0] + l0) * L1 + loc[1], wr, w[D - 1], rot);
       acc.x = fma(w[0][l0], s.x, acc.x);
       acc.y = fma(w[0][l0], s.y, acc.y);
     }
@@ -146,16 +191,7 @@ __device__ __forceinline__ typename cplx<T>::type gather_tile(const Geom& g, con
       s1.y = (T)0;
 #pragma unroll
       for (int l1 = 0; l1 < 2 * M; ++l1) {
-        const C* row = tile + ((loc[0] + l0) * L1 + loc[1] + l1) * L2 + loc[2];
-        C s;
-        s.x = (T)0;
-        s.y = (T)0;
-#pragma unroll
-        for (int l2 = 0; l2 < 2 * M; ++l2) {
-          const C v = row[l2];
-          s.x = fma(w[2][l2], v.x, s.x);
-          s.y = fma(w[2][l2], v.y, s.y);
-        }
+        const C s = row_sum<T, M>(tile + ((loc[0] + l0) * L1 + loc[1] + l1) * L2 + loc[2], wr, w[D - 1], rot);
         s1.x = fma(w[1][l1], s.x, s1.x);
         s1.y = fma(w[1][l1], s.y, s1.y);
       }
@@ -455,6 +491,573 @@ __global__ void __launch_bounds__(LocCfg<T, D, M>::THR) spread_loc_kernel(
       for_region<D>(g, tc, [&](int r, long long o) {
         const C x = acc[r];
         if (x.x != (T)0 || x.y != (T)0) red_add<T>(dst + o, x);
+      });
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------ adjoint, owner-computes
+// One CTA per tile writes exactly the tile's Q^D grid cells, once, with plain
+// coalesced stores: no zero pass, no global atomics. The
+// CTA gathers every node of its 3^D neighbour tiles whose footprint reaches
+// into the tile (Q_d | Ntilde_d, P_d >= 3, Q_d >= 2m), buckets them by 2m-wide
+// sub-tiles of an extended sub-tile grid (one ring outside the tile), and
+// accumulates the clipped footprints with the coloured lanes-own-cells scheme
+// of spread_loc_kernel. Empty tiles just write zeros.
+template <typename T, int D, int M>
+struct OwnCfg {
+  static constexpr int THR = D == 1 ? 256 : 128;
+  static constexpr int LISTCAP = 2048;
+};
+
+template <typename T, int D, int M, int DEG>
+__global__ void __launch_bounds__(OwnCfg<T, D, M>::THR) spread_own_kernel(
+    Geom g, WinPoly<T> wp, const typename cplx<T>::type* __restrict__ f, const T* __restrict__ ks,
+    const int* __restrict__ perm, const int* __restrict__ offsets, int nb, int ne,
+    typename cplx<T>::type* __restrict__ grid) {
+  using C = typename cplx<T>::type;
+  using L = LocCfg<T, D, M>;
+  constexpr int TAPS = L::TAPS, F = L::F, G = L::G, STEPS = L::STEPS;
+  constexpr int THR = OwnCfg<T, D, M>::THR, LISTCAP = OwnCfg<T, D, M>::LISTCAP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int tile_cells = 1, NSX[MAX_D], nst = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    tile_cells *= g.Q[d];
+    NSX[d] = (g.Q[d] + TAPS - 1) / TAPS + 2;  // extended sub-tile grid
+    nst *= NSX[d];
+  }
+  C* acc = reinterpret_cast<C*>(smem_raw);
+  T* tap = reinterpret_cast<T*>(acc + tile_cells);  // [THR][D][TAPS]
+  size_t off = ((size_t)tile_cells * sizeof(C) + (size_t)THR * D * TAPS * sizeof(T) + 15) & ~(size_t)15;
+  C* fv = reinterpret_cast<C*>(smem_raw + off);
+  int* jv = reinterpret_cast<int*>(fv + THR);
+  int* order = jv + THR;
+  int* sv = order + THR;        // [D][THR] footprint start relative to the tile origin
+  int* list = sv + D * THR;     // [LISTCAP]
+  int* stoff = list + LISTCAP;  // [nst + 1]
+  int* stcur = stoff + nst + 1; // [nst]
+  int* counters = stcur + nst;  // [0] list length
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lg = lane % G;
+  const bool worker_lane = lane < L::WPW * G;
+  const int worker = worker_lane ? warp * L::WPW + lane / G : 1 << 30;
+  const int nworkers = (THR >> 5) * L::WPW;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane / G * G));
+  int strides[MAX_D];
+  strides[D - 1] = 1;
+#pragma unroll
+  for (int d = D - 2; d >= 0; --d) strides[d] = strides[d + 1] * g.Q[d + 1];
+  int ntiles = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) ntiles *= g.P[d];
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int p[MAX_D];
+    {
+      int rem = tile;
+#pragma unroll
+      for (int d = D - 1; d >= 0; --d) {
+        p[d] = rem % g.P[d];
+        rem /= g.P[d];
+      }
+    }
+    for (int b = 0; b < g.B; ++b) {
+      for (int r = threadIdx.x; r < tile_cells; r += THR) {
+        acc[r].x = (T)0;
+        acc[r].y = (T)0;
+      }
+      // walk the 3^D neighbour tiles; relevant nodes are compacted into `list`
+      // and consumed in chunks of THR nodes
+      int nbhd = 1;
+#pragma unroll
+      for (int d = 0; d < D; ++d) nbhd *= 3;
+      for (int nbi = 0; nbi < nbhd; ++nbi) {
+        int q = 0, dl[MAX_D], qo[MAX_D];  // qo: cell origin of the (wrapped) neighbour tile minus dl*Q
+        {
+          int rem = nbi;
+#pragma unroll
+          for (int d = D - 1; d >= 0; --d) {
+            dl[d] = rem % 3 - 1;
+            rem /= 3;
+          }
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            int qd = p[d] + dl[d];
+            qd = qd < 0 ? qd + g.P[d] : (qd >= g.P[d] ? qd - g.P[d] : qd);
+            q = q * g.P[d] + qd;
+            qo[d] = qd * g.Q[d] - dl[d] * g.Q[d];
+          }
+        }
+        const int i0 = max(offsets[q], nb), i1 = min(offsets[q + 1], ne);
+        for (int cbase = i0; cbase < i1; cbase += LISTCAP) {
+          const int cend = min(i1, cbase + LISTCAP);
+          if (threadIdx.x == 0) counters[0] = 0;
+          __syncthreads();
+          for (int i = cbase + threadIdx.x; i < cend; i += THR) {
+            bool rel = true;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+              double frac;
+              const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
+              const int s0 = c - qo[d] - M + 1;  // footprint start relative to this tile (unwrapped)
+              rel = rel && s0 < g.Q[d] && s0 + TAPS > 0;
+            }
+            if (rel) list[atomicAdd(&counters[0], 1)] = i;
+          }
+          __syncthreads();
+          const int nlist = counters[0];
+          for (int lb = 0; lb < nlist; lb += THR) {
+            const int nchunk = min(THR, nlist - lb);
+            for (int i = threadIdx.x; i <= nst; i += THR) stoff[i] = 0;
+            __syncthreads();
+            int st = 0;
+            if (threadIdx.x < nchunk) {
+              const int t = threadIdx.x;
+              const int i = list[lb + t];
+              jv[t] = perm[i];
+#pragma unroll
+              for (int d = 0; d < D; ++d) {
+                double frac;
+                const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
+                const int rel = c - qo[d];
+                sv[d * THR + t] = rel - M + 1;
+                st = st * NSX[d] + (rel >= 0 ? rel / TAPS + 1 : 0);
+                T w[TAPS];
+                window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w);
+#pragma unroll
+                for (int l = 0; l < TAPS; ++l) tap[(t * D + d) * TAPS + l] = w[l];
+              }
+              fv[t] = f[(long long)b * g.M + jv[t]];
+              atomicAdd(&stoff[st + 1], 1);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+              for (int k = 1; k <= nst; ++k) stoff[k] += stoff[k - 1];
+            __syncthreads();
+            for (int k = threadIdx.x; k < nst; k += THR) stcur[k] = stoff[k];
+            __syncthreads();
+            if (threadIdx.x < nchunk) order[atomicAdd(&stcur[st], 1)] = threadIdx.x;
+            __syncthreads();
+            for (int color = 0; color < (1 << D); ++color) {
+              int cnt[MAX_D], nu = 1;
+#pragma unroll
+              for (int d = 0; d < D; ++d) {
+                const int par = (color >> (D - 1 - d)) & 1;
+                cnt[d] = (NSX[d] - par + 1) / 2;
+                nu *= cnt[d];
+              }
+              for (int u = worker; u < nu; u += nworkers) {
+                int sti = 0, rem = u, ud[MAX_D];
+#pragma unroll
+                for (int d = D - 1; d >= 0; --d) {
+                  ud[d] = rem % cnt[d];
+                  rem /= cnt[d];
+                }
+#pragma unroll
+                for (int d = 0; d < D; ++d) sti = sti * NSX[d] + 2 * ud[d] + ((color >> (D - 1 - d)) & 1);
+                const int q1 = stoff[sti + 1];
+                for (int qq = stoff[sti]; qq < q1; ++qq) {
+                  const int t = order[qq];
+                  const C v = fv[t];
+                  int s0[MAX_D];
+#pragma unroll
+                  for (int d = 0; d < D; ++d) s0[d] = sv[d * THR + t];
+                  const T* tp = tap + t * D * TAPS;
+#pragma unroll
+                  for (int s2 = 0; s2 < STEPS; ++s2) {
+                    const int c = lg + G * s2;
+                    if (F % G == 0 || c < F) {
+                      T w = (T)1;
+                      int a = 0, rc = c;
+                      bool in = true;
+#pragma unroll
+                      for (int d = D - 1; d >= 0; --d) {
+                        const int l = rc % TAPS;
+                        rc /= TAPS;
+                        const int x = s0[d] + l;
+                        in = in && x >= 0 && x < g.Q[d];
+                        w *= tp[d * TAPS + l];
+                        a += x * strides[d];
+                      }
+                      if (in) {
+                        C x = acc[a];
+                        x.x = fma(w, v.x, x.x);
+                        x.y = fma(w, v.y, x.y);
+                        acc[a] = x;
+                      }
+                    }
+                  }
+                  __syncwarp(gmask);
+                }
+              }
+              __syncthreads();
+            }
+          }
+        }
+      }
+      // write the tile: rows along the contiguous last dimension
+      C* dst = grid + (long long)b * g.grid_cells;
+      const int Ql = g.Q[D - 1];
+      const int rows = tile_cells / Ql;
+      for (int r = threadIdx.x / 32; r < rows; r += THR / 32) {
+        long long rowoff = 0;
+        int rr = r;
+        int idx[MAX_D];
+#pragma unroll
+        for (int d = D - 2; d >= 0; --d) {
+          idx[d] = rr % g.Q[d];
+          rr /= g.Q[d];
+        }
+#pragma unroll
+        for (int d = 0; d < D - 1; ++d) {
+          int sd = p[d] * g.Q[d] + idx[d] + (g.Nt[d] >> 1);
+          if (sd >= g.Nt[d]) sd -= g.Nt[d];
+          rowoff = rowoff * g.Nt[d] + sd;
+        }
+        rowoff *= g.Nt[D - 1];
+        const int base = p[D - 1] * Ql + (g.Nt[D - 1] >> 1);
+        for (int x = lane; x < Ql; x += 32) {
+          int sx = base + x;
+          if (sx >= g.Nt[D - 1]) sx -= g.Nt[D - 1];
+          dst[rowoff + sx] = acc[r * Ql + x];
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------ adjoint, cell-sorted warp chunks
+// Thread-per-node spreading without shared-memory atomics:
+//  1. the subproblem's nodes are counting-sorted by their local cell (row-major
+//     in the tile) in shared memory;
+//  2. sorted node s belongs to lane s%32 of warp-chunk s/32. Lanes of one chunk
+//     add the same tap offset in the same instruction, so they can only collide
+//     when two nodes share a cell; those are serialised by their rank among the
+//     equal-cell lanes (__match_any_sync). Across instructions, the lanes' plain
+//     read-modify-writes are ordered by `volatile` shared accesses of a
+//     converged warp;
+//  3. chunks whose footprint row ranges (dimension 0) overlap never run at the
+//     same time: chunk k runs in phase k mod K, K = 1 + the most later chunks
+//     any chunk overlaps with (computed per subproblem, so dense clusters just
+//     serialise more);
+//  4. the tile region is flushed with global reductions (Alg. 4's merge).
+template <typename T, int D, int M, int DEG>
+__global__ void __launch_bounds__(THREADS) spread_sorted_kernel(Geom g, WinPoly<T> wp,
+                                                                const typename cplx<T>::type* __restrict__ f,
+                                                                const T* __restrict__ ks, const int* __restrict__ perm,
+                                                                const int4* __restrict__ subs,
+                                                                const int* __restrict__ nsub_ptr,
+                                                                typename cplx<T>::type* __restrict__ grid) {
+  using C = typename cplx<T>::type;
+  constexpr int TAPS = 2 * M;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int tile_cells = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) tile_cells *= g.Q[d];
+  C* tile = reinterpret_cast<C*>(smem_raw);
+  int* hist = reinterpret_cast<int*>(tile + g.region_cells);  // [tile_cells + 1]
+  int* order = hist + tile_cells + 1;                         // [THREADS] sorted slot -> subproblem index
+  int* rows = order + THREADS;                                // [2 * 8] first/last row of every chunk
+  int* kshared = rows + 16;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int rstr[MAX_D];  // region strides
+  rstr[D - 1] = 1;
+#pragma unroll
+  for (int d = D - 2; d >= 0; --d) rstr[d] = rstr[d + 1] * g.L[d + 1];
+
+  const int nsub = *nsub_ptr;
+  for (int s = blockIdx.x; s < nsub; s += gridDim.x) {
+    const int4 sp = subs[s];
+    const TileCoords tc = tile_coords<D, M>(g, sp.x);
+    for (int i = threadIdx.x; i <= tile_cells; i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) kshared[0] = 1;
+    __syncthreads();
+    // 1. local cell of every node, histogram
+    int lc = -1;
+    if (threadIdx.x < sp.z) {
+      const int i = sp.y + threadIdx.x;
+      lc = 0;
+      bool ok = true;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double frac;
+        const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
+        const int loc = c - tc.p[d] * g.Q[d];
+        ok = ok && (unsigned)loc < (unsigned)g.Q[d];
+        lc = lc * g.Q[d] + (ok ? loc : 0);
+      }
+      if (!ok) lc = -1;
+      else atomicAdd(&hist[lc + 1], 1);
+    }
+    __syncthreads();
+    // exclusive scan of the cell histogram (tile_cells + 1 entries)
+    {
+      __shared__ int ws[32];
+      const int per = (tile_cells + 1 + blockDim.x - 1) / blockDim.x;
+      const int lo = threadIdx.x * per, hi = min(tile_cells + 1, lo + per);
+      int sum = 0;
+      for (int k = lo; k < hi; ++k) sum += hist[k];
+      int total;
+      int run = block_exclusive_scan(sum, ws, total);
+      for (int k = lo; k < hi; ++k) {
+        run += hist[k];
+        hist[k] = run;  // inclusive of hist[k] (hist[0] = 0): hist[lc] = start of cell lc
+      }
+    }
+    __syncthreads();
+    int nvalid = hist[tile_cells];
+    if (lc >= 0) order[atomicAdd(&hist[lc], 1)] = threadIdx.x;
+    __syncthreads();
+    // 2. sorted slot -> node data and taps in registers
+    const int slot = threadIdx.x;
+    const bool has = slot < nvalid;
+    int j = 0, loc[D], mycell = -1;
+    T w[D][TAPS];
+    if (has) {
+      const int t = order[slot];
+      const int i = sp.y + t;
+      j = perm[i];
+      mycell = 0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double frac;
+        const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
+        loc[d] = c - tc.p[d] * g.Q[d];
+        mycell = mycell * g.Q[d] + loc[d];
+        window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w[d]);
+      }
+    }
+    // 3. chunk row ranges and the number of phases K
+    const int nchunks = (nvalid + 31) / 32;
+    if (has && (lane == 0 || slot == nvalid - 1 || lane == 31)) {
+      if (lane == 0) rows[2 * warp] = loc[0];
+      if (lane == 31 || slot == nvalid - 1) rows[2 * warp + 1] = loc[0];
+    }
+    __syncthreads();
+    if (threadIdx.x < nchunks) {
+      const int k = threadIdx.x;
+      int cnt = 0;
+      for (int k2 = k + 1; k2 < nchunks; ++k2) {
+        if (rows[2 * k2] - rows[2 * k + 1] <= 2 * M - 1) ++cnt;  // footprint rows overlap
+        else break;
+      }
+      atomicMax(&kshared[0], cnt + 1);
+    }
+    __syncthreads();
+    const int K = kshared[0];
+    // duplicate-cell rank inside the warp
+    const unsigned peers = __match_any_sync(0xffffffffu, has ? mycell : -1 - lane);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    int rounds = __reduce_max_sync(0xffffffffu, has ? rank + 1 : 0);
+    int base = 0;
+    if (has) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) base += loc[d] * rstr[d];
+    }
+    for (int b = 0; b < g.B; ++b) {
+      for (int r = threadIdx.x; r < g.region_cells; r += blockDim.x) {
+        tile[r].x = (T)0;
+        tile[r].y = (T)0;
+      }
+      C v;
+      v.x = (T)0;
+      v.y = (T)0;
+      if (has) v = f[(long long)b * g.M + j];
+      __syncthreads();
+      volatile T* vt = reinterpret_cast<volatile T*>(tile);
+      for (int ph = 0; ph < K; ++ph) {
+        if (warp < nchunks && warp % K == ph) {
+          for (int rd = 0; rd < rounds; ++rd) {
+            if (has && rank == rd) {
+              if (D == 1) {
+#pragma unroll
+                for (int l = 0; l < TAPS; ++l) {
+                  const int a = 2 * (base + l);
+                  vt[a] = fma(w[0][l], v.x, vt[a]);
+                  vt[a + 1] = fma(w[0][l], v.y, vt[a + 1]);
+                }
+              } else if (D == 2) {
+#pragma unroll
+                for (int l0 = 0; l0 < TAPS; ++l0) {
+                  const T ax = w[0][l0] * v.x, ay = w[0][l0] * v.y;
+#pragma unroll
+                  for (int l1 = 0; l1 < TAPS; ++l1) {
+                    const int a = 2 * (base + l0 * rstr[0] + l1);
+                    vt[a] = fma(w[1][l1], ax, vt[a]);
+                    vt[a + 1] = fma(w[1][l1], ay, vt[a + 1]);
+                  }
+                }
+              } else {
+                constexpr int U0 = (2 * M <= 8) ? 2 * M : 1;
+#pragma unroll U0
+                for (int l0 = 0; l0 < TAPS; ++l0) {
+                  const T ax0 = w[0][l0] * v.x, ay0 = w[0][l0] * v.y;
+#pragma unroll
+                  for (int l1 = 0; l1 < TAPS; ++l1) {
+                    const T ax = w[1][l1] * ax0, ay = w[1][l1] * ay0;
+#pragma unroll
+                    for (int l2 = 0; l2 < TAPS; ++l2) {
+                      const int a = 2 * (base + l0 * rstr[0] + l1 * rstr[1] + l2);
+                      vt[a] = fma(w[2][l2], ax, vt[a]);
+                      vt[a + 1] = fma(w[2][l2], ay, vt[a + 1]);
+                    }
+                  }
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+      }
+      C* dst = grid + (long long)b * g.grid_cells;
+      for_region<D>(g, tc, [&](int r, long long o) {
+        const C x = tile[r];
+        if (x.x != (T)0 || x.y != (T)0) red_add<T>(dst + o, x);
+      });
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------ adjoint, cell gather (default for D <= 2)
+// Spreading computed as a gather: the subproblem's nodes
+// are counting-sorted by their local cell in shared memory (taps evaluated once
+// per node, even/odd polynomial, stored with the node); then every region cell
+// x is produced by ONE thread as sum_j f_j psi~(k_j - x/Nt) over the nodes whose
+// cells lie in [x - m, x + m - 1] per dimension — contiguous ranges of the
+// cell-sorted list (one range per row in 2D). No shared-memory read-modify-
+// write, no atomics inside the CTA; each region cell is reduced into the grid
+// once (coalesced global reduction, Alg. 4's merge).
+template <typename T, int D, int M, int DEG>
+__global__ void __launch_bounds__(THREADS) spread_gather_kernel(Geom g, WinPoly<T> wp,
+                                                                const typename cplx<T>::type* __restrict__ f,
+                                                                const T* __restrict__ ks, const int* __restrict__ perm,
+                                                                const int4* __restrict__ subs,
+                                                                const int* __restrict__ nsub_ptr, int S,
+                                                                typename cplx<T>::type* __restrict__ grid) {
+  using C = typename cplx<T>::type;
+  constexpr int TAPS = 2 * M;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int tile_cells = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) tile_cells *= g.Q[d];
+  T* tap = reinterpret_cast<T*>(smem_raw);  // [S][D][TAPS]
+  size_t off = ((size_t)S * D * TAPS * sizeof(T) + 15) & ~(size_t)15;
+  C* fv = reinterpret_cast<C*>(smem_raw + off);
+  int* cl = reinterpret_cast<int*>(fv + S);  // [D][S] local cell of the slot
+  int* js = cl + D * S;                      // [S]
+  int* start = js + S;                       // [tile_cells + 1]
+  int* cursor = start + tile_cells + 1;      // [tile_cells + 1]
+  __shared__ int ws[32];
+
+  const int nsub = *nsub_ptr;
+  for (int sidx = blockIdx.x; sidx < nsub; sidx += gridDim.x) {
+    const int4 sp = subs[sidx];
+    const TileCoords tc = tile_coords<D, M>(g, sp.x);
+    for (int i = threadIdx.x; i <= tile_cells; i += blockDim.x) start[i] = 0;
+    __syncthreads();
+    // 1. cells + histogram (node t of the subproblem handled by thread t, looping)
+    for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
+      const int i = sp.y + t;
+      int lc = 0;
+      bool ok = true;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double frac;
+        const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
+        const int loc = c - tc.p[d] * g.Q[d];
+        ok = ok && (unsigned)loc < (unsigned)g.Q[d];
+        lc = lc * g.Q[d] + (ok ? loc : 0);
+      }
+      if (ok) atomicAdd(&start[lc + 1], 1);
+    }
+    __syncthreads();
+    {
+      const int per = (tile_cells + 1 + blockDim.x - 1) / blockDim.x;
+      const int lo = threadIdx.x * per, hi = min(tile_cells + 1, lo + per);
+      int sum = 0;
+      for (int k = lo; k < hi; ++k) sum += start[k];
+      int total;
+      int run = block_exclusive_scan(sum, ws, total);
+      for (int k = lo; k < hi; ++k) {
+        run += start[k];
+        start[k] = run;  // start[c] = first slot of local cell c; start[tile_cells] = count
+        cursor[k] = run;
+      }
+    }
+    __syncthreads();
+    // 2. sorted slots: taps, cells, node index
+    for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
+      const int i = sp.y + t;
+      int loc[D], lc = 0;
+      bool ok = true;
+      T w[D][TAPS];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double frac;
+        const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
+        loc[d] = c - tc.p[d] * g.Q[d];
+        ok = ok && (unsigned)loc[d] < (unsigned)g.Q[d];
+        lc = lc * g.Q[d] + (ok ? loc[d] : 0);
+        window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w[d]);
+      }
+      if (!ok) continue;
+      const int slot = atomicAdd(&cursor[lc], 1);
+      js[slot] = perm[i];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        cl[d * S + slot] = loc[d];
+#pragma unroll
+        for (int l = 0; l < TAPS; ++l) tap[(slot * D + d) * TAPS + l] = w[d][l];
+      }
+    }
+    __syncthreads();
+    const int nvalid = start[tile_cells];
+    // 3. per batch vector: every region cell gathered by one thread, reduced into the grid
+    for (int b = 0; b < g.B; ++b) {
+      for (int q = threadIdx.x; q < nvalid; q += blockDim.x) fv[q] = f[(long long)b * g.M + js[q]];
+      __syncthreads();
+      C* dst = grid + (long long)b * g.grid_cells;
+      for_region<D>(g, tc, [&](int r, long long o) {
+        C acc;
+        acc.x = (T)0;
+        acc.y = (T)0;
+        if (D == 1) {
+          const int x = r - (M - 1);  // tile-relative cell of region index r
+          const int c_lo = max(0, x - M), c_hi = min(g.Q[0] - 1, x + M - 1);
+          if (c_lo <= c_hi) {
+            const int q1 = start[c_hi + 1];
+            for (int q = start[c_lo]; q < q1; ++q) {
+              const T wt = tap[q * TAPS + (x - cl[q] + M - 1)];
+              const C v = fv[q];
+              acc.x = fma(wt, v.x, acc.x);
+              acc.y = fma(wt, v.y, acc.y);
+            }
+          }
+        } else {
+          const int L1 = g.L[1];
+          const int x0 = r / L1 - (M - 1), x1 = r % L1 - (M - 1);
+          const int r_lo = max(0, x0 - M), r_hi = min(g.Q[0] - 1, x0 + M - 1);
+          const int c_lo = max(0, x1 - M), c_hi = min(g.Q[1] - 1, x1 + M - 1);
+          if (c_lo <= c_hi) {
+            for (int c0 = r_lo; c0 <= r_hi; ++c0) {
+              const int q1 = start[c0 * g.Q[1] + c_hi + 1];
+              const int l0 = x0 - c0 + M - 1;
+              for (int q = start[c0 * g.Q[1] + c_lo]; q < q1; ++q) {
+                const T wt = tap[(q * 2) * TAPS + l0] * tap[(q * 2 + 1) * TAPS + (x1 - cl[S + q] + M - 1)];
+                const C v = fv[q];
+                acc.x = fma(wt, v.x, acc.x);
+                acc.y = fma(wt, v.y, acc.y);
+              }
+            }
+          }
+        }
+        if (acc.x != (T)0 || acc.y != (T)0) red_add<T>(dst + o, acc);
       });
       __syncthreads();
     }
