@@ -60,7 +60,7 @@ typedef enum {
   NFFT_ERROR_OUT_OF_MEMORY = 6,
   NFFT_ERROR_CUDA = 7,
   NFFT_ERROR_CUFFT = 8,
-  NFFT_ERROR_UNSUPPORTED = 9      /* D > 3, m > 8, or sizes beyond int32 indexing */
+  NFFT_ERROR_UNSUPPORTED = 9      /* D > 3, m > 8, more than 40960 tiles, or sizes beyond int32 indexing */
 } nfft_status;
 
 /* Resampling kernels. */

@@ -1,9 +1,12 @@
 // grid.cuh — resampling correction fused with zero-pad / crop (SURVEY §8(a)
-// rows a4 and a9), and grid zeroing for the adjoint.
+// rows a4 and a9).
 //
 // Oversampled-grid storage: logical l in I_Ntilde at (l mod Ntilde)_d; with it
 // the grid DFT of Alg. 1 l.5 / Alg. 2 l.5 is cuFFT's plain unnormalised
 // transform (the paper's fftshift, becomes index placement).
+// Three plan-owned grids (DESIGN.md §HBM layout): the forward input (zero
+// padding persists), the forward FFT output (out-of-place) and the adjoint
+// grid (zero between adjoints: crop_zero re-zeroes it).
 #pragma once
 
 #include "common.cuh"
@@ -22,57 +25,15 @@ __device__ __forceinline__ int decode_row(long long row, int D, const int* ext, 
 }
 
 // Alg. 1 lines 1-3 with the tensor-product correction of
-// g_n = fhat_n * prod_d beta^tensor_{n_d,d} for n in I_N, 0
-// elsewhere. grid.y walks rows of the oversampled grid (batch x all but the
-// last dimension, decoded once per CTA); grid.x the contiguous last dimension.
-// Every oversampled cell is written exactly once, coalesced.
+// g_n = fhat_n * prod_d beta^tensor_{n_d,d} for n in I_N.
+// The forward input grid keeps its zero padding between calls (the FFT is
+// out-of-place), so only the |I_N| cells are written: one thread per N-grid
+// cell, grid.y over rows (batch x all but the last dimension), grid.x over the
+// contiguous last dimension.
 template <typename T>
-__global__ void __launch_bounds__(THREADS) deconv_pad_kernel(Geom g, const typename cplx<T>::type* __restrict__ fhat,
-                                                             const T* __restrict__ beta,
-                                                             typename cplx<T>::type* __restrict__ grid) {
-  using C = typename cplx<T>::type;
-  const int D = g.D;
-  const int ntl = g.Nt[D - 1], nl = g.N[D - 1];
-  const long long rows = (long long)g.B * (g.grid_cells / ntl);
-  for (long long row = blockIdx.y; row < rows; row += gridDim.y) {
-    int s[MAX_D];
-    const int b = decode_row(row, D, g.Nt, s);
-    bool inside = true;
-    T scale = (T)1;
-    long long lin = 0;
-    for (int d = 0; d < D - 1; ++d) {
-      const int n = s[d] < (g.Nt[d] >> 1) ? s[d] : s[d] - g.Nt[d];  // logical index l in I_Ntilde
-      const int i = n + (g.N[d] >> 1);                              // N-grid storage index of n
-      inside = inside && i >= 0 && i < g.N[d];
-      if (inside) scale *= beta[g.beta_off[d] + i];
-      lin = lin * g.N[d] + i;
-    }
-    const C* src = fhat + (long long)b * g.ngrid_cells + lin * nl;
-    C* dst = grid + row * ntl;
-    const T* bl = beta + g.beta_off[D - 1];
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < ntl; x += gridDim.x * blockDim.x) {
-      const int n = x < (ntl >> 1) ? x : x - ntl;
-      const int i = n + (nl >> 1);
-      C out;
-      out.x = (T)0;
-      out.y = (T)0;
-      if (inside && i >= 0 && i < nl) {
-        const C v = src[i];
-        const T sc = scale * bl[i];
-        out.x = v.x * sc;
-        out.y = v.y * sc;
-      }
-      dst[x] = out;
-    }
-  }
-}
-
-// Alg. 2 lines 7-9 (PAPER.md:278-280): y_n = g_n * prod_d beta^tensor_{n_d,d},
-// n in I_N, read from (n mod Ntilde). Same row/column launch over the N-grid.
-template <typename T>
-__global__ void __launch_bounds__(THREADS) crop_deconv_kernel(Geom g, const typename cplx<T>::type* __restrict__ grid,
-                                                              const T* __restrict__ beta,
-                                                              typename cplx<T>::type* __restrict__ y) {
+__global__ void __launch_bounds__(THREADS) deconv_place_kernel(Geom g, const typename cplx<T>::type* __restrict__ fhat,
+                                                               const T* __restrict__ beta,
+                                                               typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
   const int D = g.D;
   const int ntl = g.Nt[D - 1], nl = g.N[D - 1];
@@ -84,31 +45,71 @@ __global__ void __launch_bounds__(THREADS) crop_deconv_kernel(Geom g, const type
     long long lin = 0;
     for (int d = 0; d < D - 1; ++d) {
       const int n = i[d] - (g.N[d] >> 1);
-      const int s = n < 0 ? n + g.Nt[d] : n;
+      const int s = n < 0 ? n + g.Nt[d] : n;  // storage of l = n: (n mod Ntilde)
       scale *= beta[g.beta_off[d] + i[d]];
       lin = lin * g.Nt[d] + s;
     }
-    const C* src = grid + (long long)b * g.grid_cells + lin * ntl;
-    C* dst = y + row * nl;
+    const C* src = fhat + row * nl;
+    C* dst = grid + (long long)b * g.grid_cells + lin * ntl;
     const T* bl = beta + g.beta_off[D - 1];
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nl; x += gridDim.x * blockDim.x) {
       const int n = x - (nl >> 1);
       const int s = n < 0 ? n + ntl : n;
-      const C v = src[s];
+      const C v = src[x];
       const T sc = scale * bl[x];
       C out;
       out.x = v.x * sc;
       out.y = v.y * sc;
-      dst[x] = out;
+      dst[s] = out;
     }
   }
 }
 
-// Zero the oversampled grid (B * prod Ntilde complex), 16-byte stores.
-__global__ void __launch_bounds__(THREADS) zero_kernel(float4* __restrict__ p, long long n16) {
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x)
-    p[i] = z;
+// Alg. 2 lines 7-9 (PAPER.md:278-280): y_n = g_n * prod_d beta^tensor_{n_d,d},
+// n in I_N, read from (n mod Ntilde) — fused with re-zeroing the adjoint grid
+// for the next spread (the adjoint's grid-is-zero invariant): one thread per
+// oversampled cell reads it if it is in I_N and then writes 0.
+template <typename T>
+__global__ void __launch_bounds__(THREADS) crop_zero_kernel(Geom g, typename cplx<T>::type* __restrict__ grid,
+                                                            const T* __restrict__ beta,
+                                                            typename cplx<T>::type* __restrict__ y) {
+  using C = typename cplx<T>::type;
+  const int D = g.D;
+  const int ntl = g.Nt[D - 1], nl = g.N[D - 1];
+  const long long rows = (long long)g.B * (g.grid_cells / ntl);
+  for (long long row = blockIdx.y; row < rows; row += gridDim.y) {
+    int s[MAX_D];
+    const int b = decode_row(row, D, g.Nt, s);
+    bool inside = true;
+    T scale = (T)1;
+    long long lin = 0;
+    for (int d = 0; d < D - 1; ++d) {
+      const int n = s[d] < (g.Nt[d] >> 1) ? s[d] : s[d] - g.Nt[d];
+      const int i = n + (g.N[d] >> 1);
+      inside = inside && i >= 0 && i < g.N[d];
+      if (inside) scale *= beta[g.beta_off[d] + i];
+      lin = lin * g.N[d] + i;
+    }
+    C* src = grid + row * ntl;
+    C* dst = y + (long long)b * g.ngrid_cells + lin * nl;
+    const T* bl = beta + g.beta_off[D - 1];
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < ntl; x += gridDim.x * blockDim.x) {
+      const int n = x < (ntl >> 1) ? x : x - ntl;
+      const int i = n + (nl >> 1);
+      if (inside && i >= 0 && i < nl) {
+        const C v = src[x];
+        const T sc = scale * bl[i];
+        C out;
+        out.x = v.x * sc;
+        out.y = v.y * sc;
+        dst[i] = out;
+      }
+      C z;
+      z.x = (T)0;
+      z.y = (T)0;
+      src[x] = z;
+    }
+  }
 }
 
 }  // namespace nfftb

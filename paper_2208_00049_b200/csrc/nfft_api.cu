@@ -44,8 +44,6 @@ struct nfft_plan_s {
   int node_begin = 0, node_end = 0;
   int64_t n_tiles = 1;
   int deg = 14;
-  int nbits = 0;
-  int sort_blocks = 1;
   int max_subs = 1;
   int grid_tiled = 1;     // CTAs for the tiled kernels
   int grid_loc = 0;       // CTAs for the conflict-free spread (0: not used)
@@ -66,23 +64,18 @@ struct nfft_plan_s {
   // device buffers
   void* d_nodes = nullptr;   // M*D reals (plan precision)
   void* d_ks = nullptr;      // D*M sorted reals
-  int* d_keys_a = nullptr;
-  int* d_vals_a = nullptr;
-  int* d_keys_b = nullptr;
-  int* d_vals_b = nullptr;
-  int* d_perm = nullptr;     // points at the sorted vals buffer
+  int* d_perm = nullptr;     // M: node index of every tile-sorted position
   int* d_offsets = nullptr;  // n_tiles + 1
-  int* d_hist = nullptr;     // 256 * sort_blocks
-  int* d_scan_tmp = nullptr;
   int* d_subbase = nullptr;  // n_tiles + 1 (last = number of subproblems)
   int4* d_subs = nullptr;
   int* d_err = nullptr;
-  int* d_cnt = nullptr;        // counting sort: [n_tiles][cs_nblk] per-block tile counts
+  int* d_cnt = nullptr;        // [cs_nblk][n_tiles] per-block tile counts (then their prefixes)
   int* d_tile_total = nullptr; // n_tiles
   unsigned* d_ticket = nullptr;
-  bool use_cs = true;
-  int cs_W = 8, cs_E = 2048, cs_nblk = 1;
-  void* d_grid = nullptr;    // B * prod Nt complex
+  int cs_nblk = 1;
+  void* d_grid_in = nullptr;  // B * prod Nt complex: forward input, zero padding persists
+  void* d_grid = nullptr;     // B * prod Nt complex: forward FFT output (read by interp)
+  void* d_grid_adj = nullptr; // B * prod Nt complex: adjoint grid, all zero between adjoints
   double* d_beta64 = nullptr;
   void* d_betaT = nullptr;
   double* d_poly = nullptr;  // D*2m*MAX_Z
@@ -146,8 +139,7 @@ bool is_device_pointer(const void* p) {
 }
 
 void free_all(nfft_plan p) {
-  void* bufs[] = {p->d_nodes, p->d_ks, p->d_keys_a, p->d_vals_a, p->d_keys_b, p->d_vals_b, p->d_offsets,
-                  p->d_hist, p->d_scan_tmp, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_beta64,
+  void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm};
   for (void* b : bufs)
@@ -157,31 +149,6 @@ void free_all(nfft_plan p) {
     for (auto& row : p->ev)
       for (auto& e : row)
         if (e) cudaEventDestroy(e);
-}
-
-nfft_status scan_exclusive(nfft_plan p, int* d, int n, int* tmp) {
-  const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  scan_tile_kernel<<<nb, THREADS, 0, p->stream>>>(d, d, n, nb > 1 ? tmp : nullptr);
-  ++p->launches;
-  CKL();
-  if (nb > 1) {
-    nfft_status s = scan_exclusive(p, tmp, nb, tmp + nb);
-    if (s != NFFT_SUCCESS) return s;
-    scan_add_kernel<<<nb, THREADS, 0, p->stream>>>(d, n, tmp);
-    ++p->launches;
-    CKL();
-  }
-  return NFFT_SUCCESS;
-}
-
-size_t scan_tmp_ints(int64_t n) {
-  size_t total = 0;
-  int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  while (nb > 1) {
-    total += nb;
-    nb = (nb + SCAN_TILE - 1) / SCAN_TILE;
-  }
-  return total + 64;
 }
 
 inline void rec(nfft_plan p, int which, int slot) {
@@ -320,64 +287,18 @@ nfft_status precompute_impl(nfft_plan p) {
   const int nt = (int)p->n_tiles;
   CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->stream));
   rec(p, 2, 0);
-  if (p->use_cs) {
-    // stable counting sort: 3 kernels (precompute.cuh)
-    const int thr = p->cs_W * 32;
-    cs_count_kernel<R><<<p->cs_nblk, thr, (size_t)nt * 4, p->stream>>>(
-        (const R*)p->d_nodes, p->geom, nt, p->cs_E, p->cs_nblk, p->d_cnt, p->d_err, p->d_ticket);
-    ++p->launches;
-    CKL();
-    cs_scan_kernel<<<(nt + 7) / 8, THREADS, 0, p->stream>>>(p->d_cnt, nt, p->cs_nblk, M, p->d_tile_total,
-                                                           p->d_offsets, p->d_ticket, p->node_begin, p->node_end,
-                                                           p->S, p->d_subbase, p->d_subs);
-    ++p->launches;
-    CKL();
-    cs_scatter_kernel<R><<<p->cs_nblk, thr, (size_t)p->cs_W * nt * 4, p->stream>>>(
-        (const R*)p->d_nodes, p->geom, nt, p->cs_E, p->cs_nblk, p->d_cnt, p->d_offsets, p->d_perm, (R*)p->d_ks);
-    ++p->launches;
-    CKL();
-    rec(p, 2, 1);
-    return NFFT_SUCCESS;
-  }
-  // radix fallback for very many tiles
-  const int nb_bin = (M + THREADS - 1) / THREADS;
-  bin_nodes_kernel<R><<<nb_bin, THREADS, 0, p->stream>>>((const R*)p->d_nodes, p->geom, p->d_keys_a, p->d_vals_a,
-                                                         p->d_err);
+  // stable counting sort into tiles: count, scan (+ offsets, subproblems), scatter (precompute.cuh)
+  cs_count_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, p->stream>>>((const R*)p->d_nodes, p->geom, nt,
+                                                                           p->d_cnt, p->d_err);
   ++p->launches;
   CKL();
-  int* ka = p->d_keys_a;
-  int* va = p->d_vals_a;
-  int* kb = p->d_keys_b;
-  int* vb = p->d_vals_b;
-  for (int shift = 0; shift < p->nbits; shift += 8) {
-    const int bits = std::min(8, p->nbits - shift);
-    radix_hist_kernel<<<p->sort_blocks, THREADS, 0, p->stream>>>(ka, M, shift, p->sort_blocks, p->d_hist);
-    ++p->launches;
-    CKL();
-    nfft_status s = scan_exclusive(p, p->d_hist, 256 * p->sort_blocks, p->d_scan_tmp);
-    if (s != NFFT_SUCCESS) return s;
-    radix_scatter_kernel<<<p->sort_blocks, THREADS, 0, p->stream>>>(ka, va, kb, vb, M, shift, bits, p->sort_blocks,
-                                                                      p->d_hist);
-    ++p->launches;
-    CKL();
-    std::swap(ka, kb);
-    std::swap(va, vb);
-  }
-  if (va != p->d_perm) CK(cudaMemcpyAsync(p->d_perm, va, (size_t)M * 4, cudaMemcpyDeviceToDevice, p->stream));
-  tile_offsets_kernel<<<(M + 1 + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(ka, M, nt, p->d_offsets);
+  cs_scan_kernel<<<(nt + 31) / 32, THREADS, 0, p->stream>>>(p->d_cnt, nt, p->cs_nblk, M, p->d_tile_total,
+                                                         p->d_offsets, p->d_ticket, p->node_begin, p->node_end,
+                                                         p->S, p->d_subbase, p->d_subs);
   ++p->launches;
   CKL();
-  gather_sorted_kernel<R><<<nb_bin, THREADS, 0, p->stream>>>((const R*)p->d_nodes, p->d_perm, p->geom, (R*)p->d_ks);
-  ++p->launches;
-  CKL();
-  count_subproblems_kernel<<<(nt + 1 + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
-      p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase);
-  ++p->launches;
-  CKL();
-  nfft_status s = scan_exclusive(p, p->d_subbase, nt + 1, p->d_scan_tmp);
-  if (s != NFFT_SUCCESS) return s;
-  write_subproblems_kernel<<<(nt + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
-      p->d_offsets, nt, p->node_begin, p->node_end, p->S, p->d_subbase, p->d_subs);
+  cs_scatter_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, p->stream>>>(
+      (const R*)p->d_nodes, p->geom, nt, p->d_cnt, p->d_offsets, p->d_perm, (R*)p->d_ks);
   ++p->launches;
   CKL();
   rec(p, 2, 1);
@@ -385,30 +306,31 @@ nfft_status precompute_impl(nfft_plan p) {
 }
 
 // ---- stages (each enqueues its kernels on the plan stream; device pointers) ----
-inline int elementwise_blocks(nfft_plan p, long long n) {
-  return (int)std::max<long long>(1, std::min<long long>((n + THREADS - 1) / THREADS, (long long)p->sm_count * 32));
-}
 
 template <typename T>
 nfft_status stage_deconv(nfft_plan p, const typename cplx<T>::type* fhat) {
   const Geom& g = p->geom;
-  const int nl = g.Nt[g.D - 1];
-  const long long rows = (long long)g.B * (g.grid_cells / nl);
+  const int nl = g.N[g.D - 1];
+  const long long rows = (long long)g.B * (g.ngrid_cells / nl);
   dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
-  deconv_pad_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, fhat, (const T*)p->d_betaT,
-                                                        (typename cplx<T>::type*)p->d_grid);
+  deconv_place_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, fhat, (const T*)p->d_betaT,
+                                                          (typename cplx<T>::type*)p->d_grid_in);
   ++p->launches;
   CKL();
   return NFFT_SUCCESS;
 }
 
+// forward: out-of-place grid_in -> grid (keeps grid_in's zero padding);
+// adjoint: in place on grid_adj. Unnormalised (reading R13).
 template <typename T>
 nfft_status stage_fft(nfft_plan p, int dir) {
+  void* in = dir == CUFFT_FORWARD ? p->d_grid_in : p->d_grid_adj;
+  void* out = dir == CUFFT_FORWARD ? p->d_grid : p->d_grid_adj;
   cufftResult r;
   if constexpr (sizeof(T) == 8)
-    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)p->d_grid, (cufftDoubleComplex*)p->d_grid, dir);
+    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)in, (cufftDoubleComplex*)out, dir);
   else
-    r = cufftExecC2C(p->fft, (cufftComplex*)p->d_grid, (cufftComplex*)p->d_grid, dir);
+    r = cufftExecC2C(p->fft, (cufftComplex*)in, (cufftComplex*)out, dir);
   return r == CUFFT_SUCCESS ? NFFT_SUCCESS : NFFT_ERROR_CUFFT;
 }
 
@@ -433,7 +355,7 @@ template <typename T>
 nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
-  auto* grid = (typename cplx<T>::type*)p->d_grid;
+  auto* grid = (typename cplx<T>::type*)p->d_grid_adj;  // all zero on entry (plan creation / previous crop)
   if (p->tiled && p->grid_own > 0) {
     // owner-computes: every grid cell written exactly once, no zero pass
     rec(p, 1, 1);
@@ -443,10 +365,6 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
     CKL();
     return NFFT_SUCCESS;
   }
-  const long long n16 = (long long)(p->geom.grid_cells * p->B * sizeof(typename cplx<T>::type) / 16);
-  zero_kernel<<<elementwise_blocks(p, n16), THREADS, 0, p->stream>>>((float4*)grid, n16);
-  ++p->launches;
-  CKL();
   rec(p, 1, 1);
   if (p->tiled && p->grid_gather > 0) {
     ks.spread_gather<<<p->grid_gather, THREADS, p->gather_bytes, p->stream>>>(
@@ -472,11 +390,11 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
 template <typename T>
 nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y) {
   const Geom& g = p->geom;
-  const int nl = g.N[g.D - 1];
-  const long long rows = (long long)g.B * (g.ngrid_cells / nl);
-  dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
-  crop_deconv_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, (const typename cplx<T>::type*)p->d_grid,
-                                                         (const T*)p->d_betaT, y);
+  const int ntl = g.Nt[g.D - 1];
+  const long long rows = (long long)g.B * (g.grid_cells / ntl);
+  dim3 grid((unsigned)std::min<long long>((ntl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
+  crop_zero_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, (typename cplx<T>::type*)p->d_grid_adj,
+                                                       (const T*)p->d_betaT, y);
   ++p->launches;
   CKL();
   return NFFT_SUCCESS;
@@ -673,22 +591,6 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     n_tiles *= P[d];
   }
   p->n_tiles = n_tiles;
-  p->nbits = 0;
-  while (((int64_t)1 << p->nbits) < n_tiles) ++p->nbits;
-  p->sort_blocks = (int)((M + SORT_TILE - 1) / SORT_TILE);
-  // counting-sort geometry: W warps per block so the [W][n_tiles] smem table fits 64 KB
-  p->use_cs = false;
-  for (int W = 8; W >= 1; W >>= 1) {
-    const int64_t E = (int64_t)W * 32 * CS_CHUNKS;
-    const int64_t nblk = (M + E - 1) / E;
-    if ((int64_t)W * n_tiles * 4 <= 65536 && n_tiles * nblk <= ((int64_t)1 << 23)) {
-      p->use_cs = true;
-      p->cs_W = W;
-      p->cs_E = (int)E;
-      p->cs_nblk = (int)nblk;
-      break;
-    }
-  }
   p->max_subs = (int)std::min<int64_t>((nend - opt.node_begin + p->S - 1) / p->S + n_tiles, 0x7fffffff);
   if (p->max_subs < 1) p->max_subs = 1;
 
@@ -732,35 +634,38 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
             alloc((void**)&p->d_perm, M * 4) && alloc((void**)&p->d_offsets, (n_tiles + 1) * 4) &&
             alloc((void**)&p->d_subbase, (n_tiles + 1) * 4) && alloc((void**)&p->d_subs, (size_t)p->max_subs * 16) &&
             alloc((void**)&p->d_err, 16) && alloc(&p->d_grid, (size_t)cells * p->B * csz) &&
+            alloc(&p->d_grid_in, (size_t)cells * p->B * csz) && alloc(&p->d_grid_adj, (size_t)cells * p->B * csz) &&
             alloc((void**)&p->d_beta64, boff * 8) && alloc(&p->d_betaT, boff * rs) &&
             alloc((void**)&p->d_poly, (size_t)D * 2 * m * MAX_Z * 8);
-  if (ok && p->use_cs) {
+  if (ok) {
+    p->cs_nblk = (int)((M + CS_E - 1) / CS_E);
+    if ((size_t)n_tiles * 4 > 160 * 1024 || (int64_t)n_tiles * p->cs_nblk > ((int64_t)1 << 28)) return fail(NFFT_ERROR_UNSUPPORTED);
     ok = alloc((void**)&p->d_cnt, (size_t)n_tiles * p->cs_nblk * 4) && alloc((void**)&p->d_tile_total, n_tiles * 4) &&
          alloc((void**)&p->d_ticket, 16);
-  } else if (ok) {
-    ok = alloc((void**)&p->d_keys_a, M * 4) && alloc((void**)&p->d_vals_a, M * 4) &&
-         alloc((void**)&p->d_keys_b, M * 4) && alloc((void**)&p->d_vals_b, M * 4) &&
-         alloc((void**)&p->d_hist, 256 * p->sort_blocks * 4) &&
-         alloc((void**)&p->d_scan_tmp, scan_tmp_ints(std::max<int64_t>(256 * p->sort_blocks, n_tiles + 1)) * 4);
   }
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
-  if (p->use_cs) {
-    const int bytes1 = (int)(n_tiles * 4), bytes3 = (int)(p->cs_W * n_tiles * 4);
+  {
+    const int bytes = (int)(n_tiles * 4);
     cudaError_t e = cudaSuccess;
     if (c128) {
-      e = cudaFuncSetAttribute((const void*)cs_count_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes1);
+      e = cudaFuncSetAttribute((const void*)cs_count_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       if (e == cudaSuccess)
-        e = cudaFuncSetAttribute((const void*)cs_scatter_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes3);
+        e = cudaFuncSetAttribute((const void*)cs_scatter_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     } else {
-      e = cudaFuncSetAttribute((const void*)cs_count_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes1);
+      e = cudaFuncSetAttribute((const void*)cs_count_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       if (e == cudaSuccess)
-        e = cudaFuncSetAttribute((const void*)cs_scatter_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes3);
+        e = cudaFuncSetAttribute((const void*)cs_scatter_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     }
     if (e != cudaSuccess) {
       last_cuda_error = e;
       return fail(NFFT_ERROR_CUDA);
     }
   }
+  if (cudaMemsetAsync(p->d_grid_in, 0, (size_t)cells * p->B * csz, p->stream) != cudaSuccess ||
+      cudaMemsetAsync(p->d_grid_adj, 0, (size_t)cells * p->B * csz, p->stream) != cudaSuccess ||
+
+      cudaMemsetAsync(p->d_ticket, 0, 16, p->stream) != cudaSuccess)
+    return fail(NFFT_ERROR_CUDA);
 
   int n[3];
   for (int d = 0; d < D; ++d) n[d] = (int)Nt[d];

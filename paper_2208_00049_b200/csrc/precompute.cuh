@@ -1,4 +1,4 @@
-// precompute.cuh — node binning, stable radix sort into tiles, subproblems
+// precompute.cuh — node binning, stable sort into tiles, subproblems
 // and window tables. All device kernels.
 //
 // PAPER.md:520-537 (block partition R_p, Gamma_p, Q = ceil(Ntilde/P)),
@@ -10,10 +10,6 @@
 
 namespace nfftb {
 
-constexpr int SORT_ITEMS = 8;
-constexpr int SORT_TILE = THREADS * SORT_ITEMS;  // 2048 keys per block
-constexpr int SCAN_ITEMS = 8;
-constexpr int SCAN_TILE = THREADS * SCAN_ITEMS;
 
 // Tile key of node j (reading R10); non-finite coordinates -> key 0, bad = true.
 template <typename R>
@@ -34,67 +30,80 @@ __device__ __forceinline__ int node_key(const R* __restrict__ nodes, const Geom&
   return bad ? 0 : key;
 }
 
-// ---------------------------------------------------------------- a1+a2: stable counting sort (3 kernels)
-// Block b of the sort owns nodes [b*E, (b+1)*E), E = 32 * W * CS_CHUNKS (W warps).
-// K1 counts tiles per block; K2 scans the [tile][block] counts (warp per tile)
-// and its last CTA scans the tile totals into the tile offsets and writes the
-// subproblem list; K3 re-walks each block in node order and places every node
-// at offsets[tile] + (nodes of that tile in earlier blocks) + (earlier nodes of
-// that tile in this block) — a stable counting sort, so perm is the unique
-// "tile ascending, original index ascending" order (reading R12). K3 also
-// writes the tile-sorted SoA coordinates.
-constexpr int CS_CHUNKS = 8;  // 32-node chunks per warp
+// ---------------------------------------------------------------- a1+a2: stable counting sort into tiles
+// Block b of the sort owns nodes [b*CS_E, (b+1)*CS_E) (CS_W warps x CS_CHUNKS
+// chunks of 32 nodes, node order = warp-major, chunk, lane).
+//  K1 cs_count:  per-block tile histogram (shared atomics) -> cnt[b][t].
+//  K2 cs_scan:   for every tile t, exclusive prefix of cnt[.][t] over blocks
+//                (one warp per tile; coalesced across warps of a CTA); the last
+//                CTA scans the tile totals into the tile offsets and writes the
+//                subproblem list (<= S nodes of one tile inside the shard).
+//  K3 cs_scatter: re-walks its block in node order; a node's position is
+//                offsets[t] + cnt[b][t] + (earlier nodes of t in this block),
+//                the last term from per-warp shared counters and warp match
+//                ranks — a stable counting sort, so perm is the unique "tile
+//                ascending, original index ascending" order (reading R12). It
+//                also writes the tile-sorted SoA coordinates.
+constexpr int CS_W = 4;
+constexpr int CS_CHUNKS = 4;
+constexpr int CS_E = CS_W * 32 * CS_CHUNKS;  // 512 nodes per sort block
 
 template <typename R>
-__global__ void cs_count_kernel(const R* __restrict__ nodes, Geom g, int n_tiles, int E, int nblk,
-                                int* __restrict__ cnt, int* __restrict__ err, unsigned* __restrict__ ticket) {
+__global__ void __launch_bounds__(CS_W * 32) cs_count_kernel(const R* __restrict__ nodes, Geom g, int n_tiles,
+                                                             int* __restrict__ cnt, int* __restrict__ err) {
   extern __shared__ int hist[];
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) hist[t] = 0;
   __syncthreads();
-  const int base = blockIdx.x * E;
+  const int base = blockIdx.x * CS_E;
   bool any_bad = false;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int j = base + e;
-    if (j >= g.M) break;
-    R k[MAX_D];
-    bool bad;
-    const int key = node_key(nodes, g, j, k, bad);
-    any_bad |= bad;
-    atomicAdd(&hist[key], 1);
+#pragma unroll
+  for (int c = 0; c < CS_CHUNKS; ++c) {
+    const int j = base + c * blockDim.x + threadIdx.x;
+    if (j < g.M) {
+      R k[MAX_D];
+      bool bad;
+      const int key = node_key(nodes, g, j, k, bad);
+      any_bad |= bad;
+      atomicAdd(&hist[key], 1);
+    }
   }
   if (any_bad) atomicOr(err, 1);
   __syncthreads();
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) cnt[(long long)t * nblk + blockIdx.x] = hist[t];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
+  int* row = cnt + (long long)blockIdx.x * n_tiles;
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) row[t] = hist[t];
 }
 
+// CTA c scans tile columns [32c, 32c + 32): lane = column, the 8 warps take
+// contiguous runs of block rows, so every global access is a coalesced
+// 128-byte row segment; a shared-memory prefix over the warps joins the runs.
 __global__ void __launch_bounds__(THREADS) cs_scan_kernel(int* __restrict__ cnt, int n_tiles, int nblk, int M,
                                                           int* __restrict__ tile_total, int* __restrict__ offsets,
                                                           unsigned* __restrict__ ticket, int nb, int ne, int S,
                                                           int* __restrict__ subbase, int4* __restrict__ subs) {
   __shared__ int ws[32];
+  __shared__ int part[THREADS / 32][33];
   __shared__ bool last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int per = (nblk + nw - 1) / nw;
+  const int r0 = warp * per, r1 = min(nblk, r0 + per);
+  int s = 0;
   if (t < n_tiles) {
-    int* row = cnt + (long long)t * nblk;
-    const int per = (nblk + 31) / 32;
-    const int lo = lane * per, hi = min(nblk, lo + per);
-    int s = 0;
-    for (int i = lo; i < hi; ++i) s += row[i];
-    int inc = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    int run = inc - s;
-    for (int i = lo; i < hi; ++i) {
-      const int c = row[i];
-      row[i] = run;
+#pragma unroll 8
+    for (int b = r0; b < r1; ++b) s += cnt[(long long)b * n_tiles + t];
+  }
+  part[warp][lane] = s;
+  __syncthreads();
+  int run = 0;
+  for (int w = 0; w < warp; ++w) run += part[w][lane];
+  if (t < n_tiles) {
+    for (int b = r0; b < r1; ++b) {
+      const long long idx = (long long)b * n_tiles + t;
+      const int c = cnt[idx];
+      cnt[idx] = run;
       run += c;
     }
-    if (lane == 31) tile_total[t] = inc;
+    if (warp == nw - 1) tile_total[t] = run;
   }
   __threadfence();
   __syncthreads();
@@ -102,22 +111,23 @@ __global__ void __launch_bounds__(THREADS) cs_scan_kernel(int* __restrict__ cnt,
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // last CTA: tile offsets = exclusive scan of the tile totals
   {
     const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
     const int lo = threadIdx.x * per, hi = min(n_tiles, lo + per);
-    int s = 0;
-    for (int i = lo; i < hi; ++i) s += __ldcg(tile_total + i);
+    int sum = 0;
+    for (int i = lo; i < hi; ++i) sum += __ldcg(tile_total + i);
     int total;
-    int run = block_exclusive_scan(s, ws, total);
+    int run = block_exclusive_scan(sum, ws, total);
     for (int i = lo; i < hi; ++i) {
       offsets[i] = run;
       run += __ldcg(tile_total + i);
     }
-    if (threadIdx.x == 0) offsets[n_tiles] = M;
+    if (threadIdx.x == 0) {
+      offsets[n_tiles] = M;
+      *ticket = 0u;
+    }
   }
   __syncthreads();
-  // subproblems: shard [nb, ne) of each tile cut into chunks of <= S nodes
   {
     const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
     const int lo = threadIdx.x * per, hi = min(n_tiles, lo + per);
@@ -138,238 +148,49 @@ __global__ void __launch_bounds__(THREADS) cs_scan_kernel(int* __restrict__ cnt,
 }
 
 template <typename R>
-__global__ void cs_scatter_kernel(const R* __restrict__ nodes, Geom g, int n_tiles, int E, int nblk,
-                                  const int* __restrict__ cnt, const int* __restrict__ offsets,
-                                  int* __restrict__ perm, R* __restrict__ ks) {
-  extern __shared__ int wb[];  // [W][n_tiles]
-  const int W = blockDim.x >> 5;
+__global__ void __launch_bounds__(CS_W * 32) cs_scatter_kernel(const R* __restrict__ nodes, Geom g, int n_tiles,
+                                                               const int* __restrict__ cnt,
+                                                               const int* __restrict__ offsets,
+                                                               int* __restrict__ perm, R* __restrict__ ks) {
+  extern __shared__ int running[];  // [n_tiles]: nodes of the tile already placed from this block
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < W * n_tiles; i += blockDim.x) wb[i] = 0;
-  __syncthreads();
-  const int base = blockIdx.x * E + warp * 32 * CS_CHUNKS;
-  int keys[CS_CHUNKS];
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) running[i] = 0;
+  const int base = blockIdx.x * CS_E;
+  const unsigned lt = (1u << lane) - 1u;
+  int keys[CS_CHUNKS], rank[CS_CHUNKS], gcount[CS_CHUNKS], pos[CS_CHUNKS];
+  bool leader[CS_CHUNKS];
   R kc[CS_CHUNKS][MAX_D];
-  int* mine = wb + warp * n_tiles;
 #pragma unroll
   for (int c = 0; c < CS_CHUNKS; ++c) {
-    const int j = base + c * 32 + lane;
+    const int j = base + c * blockDim.x + threadIdx.x;
     bool bad;
     keys[c] = j < g.M ? node_key(nodes, g, j, kc[c], bad) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, keys[c]);
-    if (keys[c] >= 0 && lane == __ffs(peers) - 1) mine[keys[c]] += __popc(peers);
-    __syncwarp();
+    rank[c] = __popc(peers & lt);
+    gcount[c] = __popc(peers);
+    leader[c] = lane == __ffs(peers) - 1;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    int run = offsets[t] + cnt[(long long)t * nblk + blockIdx.x];
-    for (int w = 0; w < W; ++w) {
-      const int c = wb[w * n_tiles + t];
-      wb[w * n_tiles + t] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
+  // groups (chunk c, warp w) in node order; each adds its counts after reading its base
 #pragma unroll
   for (int c = 0; c < CS_CHUNKS; ++c) {
-    const int key = keys[c];
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    int pos = 0;
-    if (key >= 0) pos = mine[key] + __popc(peers & lt);
-    __syncwarp();
-    if (key >= 0 && lane == __ffs(peers) - 1) mine[key] += __popc(peers);
-    __syncwarp();
-    if (key >= 0) {
-      perm[pos] = base + c * 32 + lane;
-      for (int d = 0; d < g.D; ++d) ks[(long long)d * g.M + pos] = kc[c][d];
+    for (int w = 0; w < CS_W; ++w) {
+      if (warp == w) {
+        if (keys[c] >= 0) pos[c] = running[keys[c]] + rank[c];
+        __syncwarp();
+        if (keys[c] >= 0 && leader[c]) running[keys[c]] += gcount[c];
+      }
+      __syncthreads();
     }
   }
-}
-
-// ---------------------------------------------------------------- a1 binning (radix fallback path)
-// key_j = C-order linear tile id of the cell node j starts from; vals_j = j.
-template <typename R>
-__global__ void __launch_bounds__(THREADS) bin_nodes_kernel(const R* __restrict__ nodes, Geom g,
-                                                            int* __restrict__ keys, int* __restrict__ vals,
-                                                            int* __restrict__ err) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= g.M) return;
-  int key = 0;
-  bool bad = false;
-  for (int d = 0; d < g.D; ++d) {
-    const double k = (double)nodes[(long long)j * g.D + d];
-    if (!isfinite(k)) {
-      bad = true;
-      continue;
-    }
-    double frac;
-    const int c = node_cell(k, g.Ntd[d], g.Nt[d], frac);
-    key = key * g.P[d] + c / g.Q[d];
-  }
-  if (bad) {
-    atomicOr(err, 1);
-    key = 0;
-  }
-  keys[j] = key;
-  vals[j] = j;
-}
-
-// ---------------------------------------------------------------- scan
-// Exclusive scan of int arrays (in may equal out). Block sums go to `sums`.
-__global__ void __launch_bounds__(THREADS) scan_tile_kernel(const int* in, int* out, int n, int* sums) {
-  __shared__ int ws[32];
-  const long long base = (long long)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
-  int v[SCAN_ITEMS];
-  int s = 0;
+  const int* crow = cnt + (long long)blockIdx.x * n_tiles;
 #pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; ++i) {
-    v[i] = base + i < n ? in[base + i] : 0;
-    s += v[i];
+  for (int c = 0; c < CS_CHUNKS; ++c) {
+    if (keys[c] < 0) continue;
+    const int p = offsets[keys[c]] + crow[keys[c]] + pos[c];
+    perm[p] = base + c * blockDim.x + threadIdx.x;
+    for (int d = 0; d < g.D; ++d) ks[(long long)d * g.M + p] = kc[c][d];
   }
-  int total;
-  int run = block_exclusive_scan(s, ws, total);
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; ++i) {
-    if (base + i < n) out[base + i] = run;
-    run += v[i];
-  }
-  if (sums != nullptr && threadIdx.x == 0) sums[blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(THREADS) scan_add_kernel(int* out, int n, const int* offs) {
-  const int add = offs[blockIdx.x];
-  const long long base = (long long)blockIdx.x * SCAN_TILE;
-  for (int i = threadIdx.x; i < SCAN_TILE; i += blockDim.x)
-    if (base + i < n) out[base + i] += add;
-}
-
-// ---------------------------------------------------------------- a2 radix sort
-// Stable LSD radix sort of (key, val) by key, 8-bit digits. Pass: per-block
-// digit histogram -> exclusive scan over [digit][block] -> stable scatter with
-// a block-local stable split sort. Stability makes the permutation the unique
-// "tile ascending, original index ascending" order (reading R12).
-__global__ void __launch_bounds__(THREADS) radix_hist_kernel(const int* __restrict__ keys, int n, int shift,
-                                                             int nblocks, int* __restrict__ hist) {
-  __shared__ int cnt[256];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt[i] = 0;
-  __syncthreads();
-  const long long base = (long long)blockIdx.x * SORT_TILE;
-  for (int i = threadIdx.x; i < SORT_TILE; i += blockDim.x)
-    if (base + i < n) atomicAdd(&cnt[(keys[base + i] >> shift) & 255], 1);
-  __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i * nblocks + blockIdx.x] = cnt[i];
-}
-
-__global__ void __launch_bounds__(THREADS) radix_scatter_kernel(const int* __restrict__ kin, const int* __restrict__ vin,
-                                                                int* __restrict__ kout, int* __restrict__ vout, int n,
-                                                                int shift, int bits, int nblocks,
-                                                                const int* __restrict__ offs) {
-  __shared__ int sk[SORT_TILE];
-  __shared__ int sv[SORT_TILE];
-  __shared__ int ws[32];
-  __shared__ int dstart[256];
-  const int tid = threadIdx.x;
-  const long long base = (long long)blockIdx.x * SORT_TILE;
-  const int dmask = (1 << bits) - 1;
-  int k[SORT_ITEMS], v[SORT_ITEMS];
-#pragma unroll
-  for (int i = 0; i < SORT_ITEMS; ++i) {
-    const long long idx = base + tid * SORT_ITEMS + i;
-    if (idx < n) {
-      k[i] = kin[idx];
-      v[i] = vin[idx];
-    } else {  // padding sorts last (max digit, after real elements)
-      k[i] = dmask << shift;
-      v[i] = -1;
-    }
-  }
-  // block-local stable sort by digit: `bits` one-bit stable splits (LSD)
-  for (int b = 0; b < bits; ++b) {
-    int zeros = 0;
-#pragma unroll
-    for (int i = 0; i < SORT_ITEMS; ++i) zeros += 1 - ((k[i] >> (shift + b)) & 1);
-    int Z;
-    const int zb = block_exclusive_scan(zeros, ws, Z);
-    int zrun = 0;
-#pragma unroll
-    for (int i = 0; i < SORT_ITEMS; ++i) {
-      const int f = (k[i] >> (shift + b)) & 1;
-      const int before = tid * SORT_ITEMS + i;
-      const int pos = f ? Z + (before - zb - zrun) : zb + zrun;
-      zrun += 1 - f;
-      sk[pos] = k[i];
-      sv[pos] = v[i];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < SORT_ITEMS; ++i) {
-      k[i] = sk[tid * SORT_ITEMS + i];
-      v[i] = sv[tid * SORT_ITEMS + i];
-    }
-    __syncthreads();
-  }
-  // local start of every digit: elements are now sorted by digit
-  for (int i = tid; i < 256; i += blockDim.x) dstart[i] = 0x7fffffff;
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < SORT_ITEMS; ++i) {
-    if (v[i] >= 0) atomicMin(&dstart[(k[i] >> shift) & 255], tid * SORT_ITEMS + i);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < SORT_ITEMS; ++i) {
-    if (v[i] < 0) continue;
-    const int dg = (k[i] >> shift) & 255;
-    const int rank = tid * SORT_ITEMS + i - dstart[dg];
-    const int pos = offs[dg * nblocks + blockIdx.x] + rank;
-    kout[pos] = k[i];
-    vout[pos] = v[i];
-  }
-}
-
-// Tile offsets from sorted keys: offsets[t] = first sorted position with key >= t.
-__global__ void __launch_bounds__(THREADS) tile_offsets_kernel(const int* __restrict__ skeys, int n, int n_tiles,
-                                                               int* __restrict__ offsets) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > n) return;
-  const int lo = i == 0 ? 0 : skeys[i - 1] + 1;
-  const int hi = i == n ? n_tiles : skeys[i];
-  for (int t = lo; t <= hi; ++t) offsets[t] = i;
-}
-
-// Sorted SoA coordinates ks[d][i] = nodes[perm[i]][d].
-template <typename R>
-__global__ void __launch_bounds__(THREADS) gather_sorted_kernel(const R* __restrict__ nodes, const int* __restrict__ perm,
-                                                                Geom g, R* __restrict__ ks) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.M) return;
-  const int j = perm[i];
-  for (int d = 0; d < g.D; ++d) ks[(long long)d * g.M + i] = nodes[(long long)j * g.D + d];
-}
-
-// Subproblems: the part of tile t inside the shard [nb, ne) of the sorted order,
-// cut into chunks of at most S nodes.
-__global__ void __launch_bounds__(THREADS) count_subproblems_kernel(const int* __restrict__ offsets, int n_tiles, int nb,
-                                                                    int ne, int S, int* __restrict__ nsub) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > n_tiles) return;
-  if (t == n_tiles) {
-    nsub[t] = 0;
-    return;
-  }
-  const int s = max(offsets[t], nb), e = min(offsets[t + 1], ne);
-  const int c = max(0, e - s);
-  nsub[t] = (c + S - 1) / S;
-}
-
-__global__ void __launch_bounds__(THREADS) write_subproblems_kernel(const int* __restrict__ offsets, int n_tiles, int nb,
-                                                                    int ne, int S, const int* __restrict__ subbase,
-                                                                    int4* __restrict__ subs) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
-  const int s = max(offsets[t], nb), e = min(offsets[t + 1], ne);
-  int q = subbase[t];
-  for (int st = s; st < e; st += S) subs[q++] = make_int4(t, st, min(S, e - st), 0);
 }
 
 // ---------------------------------------------------------------- a3 window tables

@@ -101,14 +101,14 @@ def test_binning_edge_nodes_1d(tile):
 
 def test_binning_all_nodes_one_tile_and_many_tiles():
     """Degenerate partitions: 4096 identical nodes (one hot tile) and
-    2^16 tiles in 2D (more radix passes)."""
+    2^15 tiles in 2D (128 KB shared histograms)."""
     nodes = np.zeros((4096, 2)) + 0.1234
     w = dict(nodes=nodes, N=(256, 256), m=4, sigma=2.0, precision="c128", batch=1)
-    plan = _plan(w, tile=(2, 2))
+    plan = _plan(w, tile=(2, 4))
     perm, offs = plan.binning()
     info = plan.info()
     plan.close()
-    assert info["n_tiles"] == 256 * 256
+    assert info["n_tiles"] == 256 * 128
     ref_perm, ref_offs, _ = obin.bin_nodes(nodes, info["Ntilde"], info["tile"])
     np.testing.assert_array_equal(perm, ref_perm)
     np.testing.assert_array_equal(offs, ref_offs)
@@ -256,7 +256,8 @@ def test_shards_sum_to_full_transform():
         out = torch.zeros((1, w["M"]), dtype=torch.complex128, device="cuda")
         plan.forward(torch.from_numpy(w["fhat"]).cuda(), out=out)
         mine = perm[rng[0]:rng[1]]
-        np.testing.assert_array_equal(out.cpu().numpy()[0, mine], full_f[0, mine])
+        # same kernels, other subproblem cuts: equal up to summation-order rounding
+        assert rel_l2(out.cpu().numpy()[0, mine], full_f[0, mine]) < 1e-15
         seen[mine] = True
         acc += plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
         plan.close()
@@ -312,3 +313,37 @@ def test_radial_clustered_c128(method):
     w = dict(nodes=nodes, N=N, m=4, sigma=2.0, precision="c128", batch=1,
              fhat=workloads.complex_normal(rng, (1,) + N), f=workloads.complex_normal(rng, (1, nodes.shape[0])))
     _check(w, method=method, tile=(16, 16))
+
+
+@pytest.mark.parametrize("method", ["tiled", "tiled_own", "direct"])
+def test_repeated_calls_and_stage_api(method):
+    """Plan scratch invariants across calls (DESIGN.md §HBM layout): the forward
+    input grid keeps its zero padding (out-of-place FFT) and the adjoint grid is
+    re-zeroed by the crop; repeated transforms with new data on one plan, and
+    the same steps through nfft_run_stage, must all match the oracle."""
+    torch = _torch()
+    w = workloads.make("cfg3_2d_512", seed=14, N=(48, 64), M=3000, m=4)
+    plan = _plan(w, method=method)
+    rng = np.random.default_rng(15)
+    for rep in range(3):
+        fhat = workloads.complex_normal(rng, (1, 48, 64))
+        f = workloads.complex_normal(rng, (1, w["M"]))
+        got_f = plan.forward(torch.from_numpy(fhat).cuda()).cpu().numpy()[0]
+        got_y = plan.adjoint(torch.from_numpy(f).cuda()).cpu().numpy()[0]
+        assert rel_l2(got_f, onfft.forward(w["nodes"], fhat[0], w["N"], 4, 2.0)) <= 1e-12
+        assert rel_l2(got_y, onfft.adjoint(w["nodes"], f[0], w["N"], 4, 2.0)) <= 1e-12
+    fhat_t = torch.from_numpy(fhat).cuda()
+    f_t = torch.from_numpy(f).cuda()
+    out_f = torch.empty((1, w["M"]), dtype=torch.complex128, device="cuda")
+    out_y = torch.empty((1, 48, 64), dtype=torch.complex128, device="cuda")
+    plan.run_stage("precompute")
+    plan.run_stage("fwd_deconv", fhat_t)
+    plan.run_stage("fwd_fft")
+    plan.run_stage("fwd_interp", None, out_f)
+    plan.run_stage("adj_spread", f_t)
+    plan.run_stage("adj_fft")
+    plan.run_stage("adj_crop", None, out_y)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out_f.cpu().numpy()[0], got_f)
+    assert rel_l2(out_y.cpu().numpy()[0], got_y) < 1e-15
+    plan.close()
