@@ -211,7 +211,8 @@ def run_reference(a):
 def config_dict(a, w, extra=None):
     d = {"workload": f"{a.config}: {len(w['N'])}D N={'x'.join(map(str, w['N']))} M={w['M']} "
                      f"{'ComplexF64' if w['precision'] == 'c128' else 'ComplexF32'} sigma={w['sigma']} m={w['m']} "
-                     f"batch={w['batch']}; step = precompute (bin+sort) + forward + adjoint",
+                     f"batch={w['batch']}; step = one nfft_execute: precompute (bin+sort) + forward + adjoint "
+                     f"(independent inputs; precompute overlaps the forward deconv+FFT, adjoint overlaps forward)",
          "nodes": "uniform i.i.d. in [-1/2,1/2)^D, seed 0", "l2": "flushed before every step (256 MiB write)",
          "parallelism": f"{'nodeshard' if a.mode == 'nodeshard' else 'independent transform per GPU'} x{a.gpus}"}
     if extra:
@@ -276,10 +277,12 @@ def main():
             flush_sink.copy_(flush_r.sum())
     flush = _Flush()
 
-    def run_steps(wk, steps, warmup, use_graph=not a.no_graph):
-        """K timed steps; each stage of the step is its own CUDA graph (or plain
-        launches with --no-graph) bracketed by CUDA events on the plan stream, so
-        the step time and every stage time are measured live."""
+    def run_steps(wk, steps, warmup, use_graph=not a.no_graph, staged=False):
+        """K timed steps. Default: the step is one nfft_execute (precompute ||
+        forward deconv+FFT, adjoint || forward, joined into the plan stream),
+        captured as one CUDA graph, timed with CUDA events on the plan stream.
+        staged=True: the stages run one after another, each in its own graph
+        between events -> live per-stage (per-kernel) durations."""
         obj, plan, nodes = build_plan(wk, False)
         with torch.cuda.stream(stream):
             fhat = torch.from_numpy(wk["fhat"]).to(dev)
@@ -289,17 +292,21 @@ def main():
         stream.synchronize()
         shard = a.mode == "nodeshard"
         from paper_2208_00049_b200.dist import allreduce_sum
-        stages = [("precompute", lambda: plan.run_stage("precompute")),
-                  ("deconv", lambda: plan.run_stage("fwd_deconv", fhat)),
-                  ("fft_fwd", lambda: plan.run_stage("fwd_fft")),
-                  ("interp", lambda: plan.run_stage("fwd_interp", None, fout))]
-        if shard:
-            stages.append(("allreduce_fwd", lambda: allreduce_sum(fout)))
-        stages += [("spread", lambda: plan.run_stage("adj_spread", f)),
-                   ("fft_adj", lambda: plan.run_stage("adj_fft")),
-                   ("crop", lambda: plan.run_stage("adj_crop", None, yout))]
-        if shard:
-            stages.append(("allreduce_adj", lambda: allreduce_sum(yout)))
+        if staged:
+            stages = [("precompute", lambda: plan.run_stage("precompute")),
+                      ("deconv", lambda: plan.run_stage("fwd_deconv", fhat)),
+                      ("fft_fwd", lambda: plan.run_stage("fwd_fft")),
+                      ("interp", lambda: plan.run_stage("fwd_interp", None, fout)),
+                      ("spread", lambda: plan.run_stage("adj_spread", f)),
+                      ("fft_adj", lambda: plan.run_stage("adj_fft")),
+                      ("crop", lambda: plan.run_stage("adj_crop", None, yout))]
+        else:
+            def one():
+                plan.execute(True, fhat, fout, f, yout)
+                if shard:
+                    allreduce_sum(fout)
+                    allreduce_sum(yout)
+            stages = [("step", one)]
         for _ in range(warmup):
             with torch.cuda.stream(stream):
                 flush.zero_()
@@ -340,7 +347,9 @@ def main():
         obj.close()
         return ms, stage, launches, clk.summary()
 
-    ms, stage, launches, clocks = run_steps(w, a.steps, a.warmup)
+    ms, _, launches, clocks = run_steps(w, a.steps, a.warmup)
+    # second timed region: the same stages one after another, for live per-kernel durations
+    ms_staged, stage, _, _ = run_steps(w, max(20, min(a.steps, 100)), a.warmup, staged=True)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -352,7 +361,8 @@ def main():
     # roofline of the dominant library kernel (by mean share of the step)
     alg = algorithmic(w)
     means = {k: (statistics.mean(v) if v else 0.0) for k, v in stage.items()}
-    mine = {k: v for k, v in means.items() if not k.startswith("fft") and not k.startswith("allreduce")}
+    # dominant single library kernel (precompute is three kernels; cuFFT is not ours)
+    mine = {k: v for k, v in means.items() if k in ("deconv", "interp", "spread", "crop")}
     dom = max(mine, key=mine.get)
     bytes_of = {"interp": alg["resample_bytes"], "spread": alg["resample_bytes"], "deconv": alg["deconv_bytes"],
                 "crop": alg["crop_bytes"], "allreduce_fwd": 0, "allreduce_adj": 0,
@@ -387,7 +397,8 @@ def main():
         sweep = {}
         for mm in range(3, 9):
             wk = workloads.make(a.config, seed=0, m=mm)
-            msk, st, _, _ = run_steps(wk, 20, 3)
+            msk, _, _, _ = run_steps(wk, 20, 3)
+            _, st, _, _ = run_steps(wk, 20, 3, staged=True)
             sweep[f"m{mm}"] = {"nodes_per_s": wk["M"] * 20 / (msk * 1e-3),
                                "interp_ms": statistics.mean(st["interp"]), "spread_ms": statistics.mean(st["spread"])}
 
@@ -403,7 +414,7 @@ def main():
             "dtype": "f64" if fp64 else "f32", "data": "synthetic",
             "config": config_dict(a, w),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "stages_ms_mean": means,
+            "stages_ms_mean": means, "ms_per_step_sequential": ms_staged / max(20, min(a.steps, 100)),
         }
         if sweep:
             line["m_sweep"] = sweep

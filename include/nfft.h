@@ -147,6 +147,20 @@ typedef enum {
 } nfft_stage;
 nfft_status nfft_run_stage(nfft_plan p, int stage, const void* in, void* out);
 
+/*
+ * Any combination of precompute, direct and adjoint NFFT in one call, with the
+ * independent pieces run concurrently on plan-internal streams: the precompute
+ * overlaps the direct NFFT's deconvolution + FFT, and the adjoint (separate
+ * scratch grid and cuFFT plan) overlaps the direct NFFT. The direct NFFT maps
+ * fhat_grid -> f_nodes and the adjoint maps the INDEPENDENT input f_in ->
+ * y_grid (f_in must not be the f_nodes of the same call). Device pointers only.
+ * All work is forked from and joined back into the plan stream (stream order
+ * and CUDA-graph capture are as for one stream-ordered call). No node check.
+ */
+typedef enum { NFFT_EXEC_PRECOMPUTE = 1, NFFT_EXEC_FORWARD = 2, NFFT_EXEC_ADJOINT = 4 } nfft_exec_flags;
+nfft_status nfft_execute(nfft_plan p, int flags, const void* fhat_grid, void* f_nodes, const void* f_in,
+                         void* y_grid);
+
 nfft_status nfft_plan_destroy(nfft_plan p);
 const char* nfft_status_string(nfft_status s);
 

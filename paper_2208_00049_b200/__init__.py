@@ -26,7 +26,7 @@ NFFT_SYMBOLS = (
     "nfft_default_options", "nfft_plan_create", "nfft_plan_create_ex", "nfft_set_nodes",
     "nfft_precompute", "nfft_forward", "nfft_adjoint", "nfft_plan_destroy", "nfft_status_string",
     "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
-    "nfft_get_launch_count", "nfft_run_stage",
+    "nfft_get_launch_count", "nfft_run_stage", "nfft_execute",
 )
 STAGES = {"precompute": 0, "fwd_deconv": 1, "fwd_fft": 2, "fwd_interp": 3, "adj_spread": 4, "adj_fft": 5,
           "adj_crop": 6}
@@ -85,6 +85,7 @@ def lib():
         "nfft_get_stage_times": [vp, c_int, P(ctypes.c_float)],
         "nfft_get_launch_count": [vp, P(i64)],
         "nfft_run_stage": [vp, c_int, vp, vp],
+        "nfft_execute": [vp, c_int, vp, vp, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -235,6 +236,29 @@ class NfftPlan:
         if stage == "precompute":
             self.precomputed = True
         return out
+
+    def execute(self, precompute=True, fhat=None, f_out=None, f_in=None, y_out=None):
+        """nfft_execute: precompute and/or direct (fhat -> f_out) and/or adjoint
+        (f_in -> y_out) NFFT with the independent parts run concurrently.
+        Device tensors only; outputs are allocated when not given."""
+        torch = _torch()
+        flags = 1 if precompute else 0
+        if fhat is not None:
+            flags |= 2
+            fhat = self._data_arg(fhat, self._grid_shape())
+            if f_out is None:
+                f_out = torch.empty((self.batch, self.M), dtype=self.tdtype_c, device=fhat.device)
+        if f_in is not None:
+            flags |= 4
+            f_in = self._data_arg(f_in, (self.batch, self.M))
+            if y_out is None:
+                y_out = torch.empty(self._grid_shape(), dtype=self.tdtype_c, device=f_in.device)
+        _check(lib().nfft_execute(self._h, flags, None if fhat is None else _ptr(fhat),
+                                  None if f_out is None else _ptr(f_out), None if f_in is None else _ptr(f_in),
+                                  None if y_out is None else _ptr(y_out)), "nfft_execute")
+        if precompute:
+            self.precomputed = True
+        return f_out, y_out
 
     def info(self):
         nt = (ctypes.c_int64 * 3)()

@@ -81,8 +81,12 @@ struct nfft_plan_s {
   double* d_poly = nullptr;  // D*2m*MAX_Z
   void* d_stage_grid = nullptr;   // B * prod N complex (host-pointer staging)
   void* d_stage_nodes = nullptr;  // B * M complex
-  cufftHandle fft = 0;
+  cufftHandle fft = 0;      // forward: out-of-place grid_in -> grid
   bool fft_ok = false;
+  cufftHandle fft_adj = 0;  // adjoint: in place on grid_adj (own plan: may run concurrently)
+  bool fft_adj_ok = false;
+  cudaStream_t side_pre = nullptr, side_adj = nullptr;  // nfft_execute's internal streams
+  cudaEvent_t ev_fork = nullptr, ev_pre = nullptr, ev_adj = nullptr;
   bool precomputed = false;
   cudaEvent_t ev[3][6] = {};
   bool events = false;
@@ -145,6 +149,11 @@ void free_all(nfft_plan p) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
+  if (p->fft_adj_ok) cufftDestroy(p->fft_adj);
+  for (cudaEvent_t e : {p->ev_fork, p->ev_pre, p->ev_adj})
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t st : {p->side_pre, p->side_adj})
+    if (st) cudaStreamDestroy(st);
   if (p->events)
     for (auto& row : p->ev)
       for (auto& e : row)
@@ -282,22 +291,22 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
 }
 
 template <typename R>
-nfft_status precompute_impl(nfft_plan p) {
+nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
   const int M = (int)p->M;
   const int nt = (int)p->n_tiles;
-  CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), p->stream));
+  CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), st));
   rec(p, 2, 0);
   // stable counting sort into tiles: count, scan (+ offsets, subproblems), scatter (precompute.cuh)
-  cs_count_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, p->stream>>>((const R*)p->d_nodes, p->geom, nt,
+  cs_count_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, st>>>((const R*)p->d_nodes, p->geom, nt,
                                                                            p->d_cnt, p->d_err);
   ++p->launches;
   CKL();
-  cs_scan_kernel<<<(nt + 31) / 32, THREADS, 0, p->stream>>>(p->d_cnt, nt, p->cs_nblk, M, p->d_tile_total,
+  cs_scan_kernel<<<(nt + 31) / 32, THREADS, 0, st>>>(p->d_cnt, nt, p->cs_nblk, M, p->d_tile_total,
                                                          p->d_offsets, p->d_ticket, p->node_begin, p->node_end,
                                                          p->S, p->d_subbase, p->d_subs);
   ++p->launches;
   CKL();
-  cs_scatter_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, p->stream>>>(
+  cs_scatter_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, st>>>(
       (const R*)p->d_nodes, p->geom, nt, p->d_cnt, p->d_offsets, p->d_perm, (R*)p->d_ks);
   ++p->launches;
   CKL();
@@ -308,12 +317,12 @@ nfft_status precompute_impl(nfft_plan p) {
 // ---- stages (each enqueues its kernels on the plan stream; device pointers) ----
 
 template <typename T>
-nfft_status stage_deconv(nfft_plan p, const typename cplx<T>::type* fhat) {
+nfft_status stage_deconv(nfft_plan p, const typename cplx<T>::type* fhat, cudaStream_t st) {
   const Geom& g = p->geom;
   const int nl = g.N[g.D - 1];
   const long long rows = (long long)g.B * (g.ngrid_cells / nl);
   dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
-  deconv_place_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, fhat, (const T*)p->d_betaT,
+  deconv_place_kernel<T><<<grid, THREADS, 0, st>>>(g, fhat, (const T*)p->d_betaT,
                                                           (typename cplx<T>::type*)p->d_grid_in);
   ++p->launches;
   CKL();
@@ -321,29 +330,34 @@ nfft_status stage_deconv(nfft_plan p, const typename cplx<T>::type* fhat) {
 }
 
 // forward: out-of-place grid_in -> grid (keeps grid_in's zero padding);
-// adjoint: in place on grid_adj. Unnormalised (reading R13).
+// adjoint: in place on grid_adj, with its own cuFFT plan so a forward and an
+// adjoint can run concurrently (nfft_execute). Unnormalised (PAPER.md:209,
+// 275; reading R13).
 template <typename T>
-nfft_status stage_fft(nfft_plan p, int dir) {
-  void* in = dir == CUFFT_FORWARD ? p->d_grid_in : p->d_grid_adj;
-  void* out = dir == CUFFT_FORWARD ? p->d_grid : p->d_grid_adj;
+nfft_status stage_fft(nfft_plan p, int dir, cudaStream_t st) {
+  const bool fwd = dir == CUFFT_FORWARD;
+  cufftHandle h = fwd ? p->fft : p->fft_adj;
+  if (cufftSetStream(h, st) != CUFFT_SUCCESS) return NFFT_ERROR_CUFFT;
+  void* in = fwd ? p->d_grid_in : p->d_grid_adj;
+  void* out = fwd ? p->d_grid : p->d_grid_adj;
   cufftResult r;
   if constexpr (sizeof(T) == 8)
-    r = cufftExecZ2Z(p->fft, (cufftDoubleComplex*)in, (cufftDoubleComplex*)out, dir);
+    r = cufftExecZ2Z(h, (cufftDoubleComplex*)in, (cufftDoubleComplex*)out, dir);
   else
-    r = cufftExecC2C(p->fft, (cufftComplex*)in, (cufftComplex*)out, dir);
+    r = cufftExecC2C(h, (cufftComplex*)in, (cufftComplex*)out, dir);
   return r == CUFFT_SUCCESS ? NFFT_SUCCESS : NFFT_ERROR_CUFFT;
 }
 
 template <typename T>
-nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f) {
+nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st) {
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   const auto* grid = (const typename cplx<T>::type*)p->d_grid;
   if (p->tiled) {
-    ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
+    ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
   } else {
-    ks.interp_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, grid, (const T*)p->d_ks, p->d_perm,
+    ks.interp_direct<<<p->grid_direct, THREADS, 0, st>>>(p->geom, wp, grid, (const T*)p->d_ks, p->d_perm,
                                                                p->node_begin, p->node_end, f);
   }
   ++p->launches;
@@ -352,14 +366,14 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f) {
 }
 
 template <typename T>
-nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
+nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStream_t st) {
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   auto* grid = (typename cplx<T>::type*)p->d_grid_adj;  // all zero on entry (plan creation / previous crop)
   if (p->tiled && p->grid_own > 0) {
     // owner-computes: every grid cell written exactly once, no zero pass
     rec(p, 1, 1);
-    ks.spread_own<<<p->grid_own, ks.own_threads, p->own_bytes, p->stream>>>(
+    ks.spread_own<<<p->grid_own, ks.own_threads, p->own_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, grid);
     ++p->launches;
     CKL();
@@ -367,19 +381,19 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
   }
   rec(p, 1, 1);
   if (p->tiled && p->grid_gather > 0) {
-    ks.spread_gather<<<p->grid_gather, THREADS, p->gather_bytes, p->stream>>>(
+    ks.spread_gather<<<p->grid_gather, THREADS, p->gather_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, p->S, grid);
   } else if (p->tiled && p->grid_loc == 0 && p->grid_sorted > 0) {
-    ks.spread_sorted<<<p->grid_sorted, THREADS, p->sorted_bytes, p->stream>>>(
+    ks.spread_sorted<<<p->grid_sorted, THREADS, p->sorted_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, grid);
   } else if (p->tiled && p->grid_loc > 0) {
-    ks.spread_loc<<<p->grid_loc, ks.loc_threads, p->loc_bytes, p->stream>>>(
+    ks.spread_loc<<<p->grid_loc, ks.loc_threads, p->loc_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, p->S, grid);
   } else if (p->tiled) {
-    ks.spread_tiled<<<p->grid_tiled, THREADS, p->region_bytes, p->stream>>>(
+    ks.spread_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, grid);
   } else {
-    ks.spread_direct<<<p->grid_direct, THREADS, 0, p->stream>>>(p->geom, wp, f, (const T*)p->d_ks, p->d_perm,
+    ks.spread_direct<<<p->grid_direct, THREADS, 0, st>>>(p->geom, wp, f, (const T*)p->d_ks, p->d_perm,
                                                                p->node_begin, p->node_end, grid);
   }
   ++p->launches;
@@ -388,12 +402,12 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f) {
 }
 
 template <typename T>
-nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y) {
+nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st) {
   const Geom& g = p->geom;
   const int ntl = g.Nt[g.D - 1];
   const long long rows = (long long)g.B * (g.grid_cells / ntl);
   dim3 grid((unsigned)std::min<long long>((ntl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
-  crop_zero_kernel<T><<<grid, THREADS, 0, p->stream>>>(g, (typename cplx<T>::type*)p->d_grid_adj,
+  crop_zero_kernel<T><<<grid, THREADS, 0, st>>>(g, (typename cplx<T>::type*)p->d_grid_adj,
                                                        (const T*)p->d_betaT, y);
   ++p->launches;
   CKL();
@@ -425,11 +439,11 @@ nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
     f = (C*)p->d_stage_nodes;
   }
   rec(p, 0, 0);
-  TRY(stage_deconv<T>(p, fhat));
+  TRY(stage_deconv<T>(p, fhat, p->stream));
   rec(p, 0, 1);
-  TRY(stage_fft<T>(p, CUFFT_FORWARD));
+  TRY(stage_fft<T>(p, CUFFT_FORWARD, p->stream));
   rec(p, 0, 2);
-  TRY(stage_interp<T>(p, f));
+  TRY(stage_interp<T>(p, f, p->stream));
   rec(p, 0, 3);
   if (host_out) {
     CK(cudaMemcpyAsync(f_out, f, node_bytes, cudaMemcpyDeviceToHost, p->stream));
@@ -457,11 +471,11 @@ nfft_status adjoint_impl(nfft_plan p, const void* f_in, void* y_out) {
     y = (C*)p->d_stage_grid;
   }
   rec(p, 1, 0);
-  TRY(stage_spread<T>(p, f));
+  TRY(stage_spread<T>(p, f, p->stream));
   rec(p, 1, 2);
-  TRY(stage_fft<T>(p, CUFFT_INVERSE));
+  TRY(stage_fft<T>(p, CUFFT_INVERSE, p->stream));
   rec(p, 1, 3);
-  TRY(stage_crop<T>(p, y));
+  TRY(stage_crop<T>(p, y, p->stream));
   rec(p, 1, 4);
   if (host_out) {
     CK(cudaMemcpyAsync(y_out, y, grid_bytes_out, cudaMemcpyDeviceToHost, p->stream));
@@ -474,14 +488,50 @@ template <typename T>
 nfft_status run_stage_impl(nfft_plan p, int stage, const void* in, void* out) {
   using C = typename cplx<T>::type;
   switch (stage) {
-    case NFFT_STAGE_FWD_DECONV: return stage_deconv<T>(p, (const C*)in);
-    case NFFT_STAGE_FWD_FFT: return stage_fft<T>(p, CUFFT_FORWARD);
-    case NFFT_STAGE_FWD_INTERP: return stage_interp<T>(p, (C*)out);
-    case NFFT_STAGE_ADJ_SPREAD: return stage_spread<T>(p, (const C*)in);
-    case NFFT_STAGE_ADJ_FFT: return stage_fft<T>(p, CUFFT_INVERSE);
-    case NFFT_STAGE_ADJ_CROP: return stage_crop<T>(p, (C*)out);
+    case NFFT_STAGE_FWD_DECONV: return stage_deconv<T>(p, (const C*)in, p->stream);
+    case NFFT_STAGE_FWD_FFT: return stage_fft<T>(p, CUFFT_FORWARD, p->stream);
+    case NFFT_STAGE_FWD_INTERP: return stage_interp<T>(p, (C*)out, p->stream);
+    case NFFT_STAGE_ADJ_SPREAD: return stage_spread<T>(p, (const C*)in, p->stream);
+    case NFFT_STAGE_ADJ_FFT: return stage_fft<T>(p, CUFFT_INVERSE, p->stream);
+    case NFFT_STAGE_ADJ_CROP: return stage_crop<T>(p, (C*)out, p->stream);
   }
   return NFFT_ERROR_INVALID_VALUE;
+}
+
+// nfft_execute: any of {precompute, forward, adjoint} with the independent
+// pieces overlapped. Precompute runs on side_pre concurrently with the
+// forward's deconvolution + FFT on the plan stream; the adjoint runs on
+// side_adj concurrently with the forward (disjoint scratch grids, own cuFFT
+// plan); interpolation and spreading wait for the precompute. Everything is
+// forked from and joined back into the plan stream, so stream order and CUDA
+// graph capture behave as for one stream-ordered call.
+template <typename T>
+nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, const void* f_in, void* y_out) {
+  using C = typename cplx<T>::type;
+  const bool pre = flags & NFFT_EXEC_PRECOMPUTE, fwd = flags & NFFT_EXEC_FORWARD, adj = flags & NFFT_EXEC_ADJOINT;
+  CK(cudaEventRecord(p->ev_fork, p->stream));
+  if (pre) {
+    CK(cudaStreamWaitEvent(p->side_pre, p->ev_fork, 0));
+    TRY(precompute_impl<T>(p, p->side_pre));
+    CK(cudaEventRecord(p->ev_pre, p->side_pre));
+  }
+  if (adj) {
+    CK(cudaStreamWaitEvent(p->side_adj, p->ev_fork, 0));
+    if (pre) CK(cudaStreamWaitEvent(p->side_adj, p->ev_pre, 0));
+    TRY(stage_spread<T>(p, (const C*)f_in, p->side_adj));
+    TRY(stage_fft<T>(p, CUFFT_INVERSE, p->side_adj));
+    TRY(stage_crop<T>(p, (C*)y_out, p->side_adj));
+    CK(cudaEventRecord(p->ev_adj, p->side_adj));
+  }
+  if (fwd) {
+    TRY(stage_deconv<T>(p, (const C*)fhat, p->stream));
+    TRY(stage_fft<T>(p, CUFFT_FORWARD, p->stream));
+    if (pre) CK(cudaStreamWaitEvent(p->stream, p->ev_pre, 0));
+    TRY(stage_interp<T>(p, (C*)f_out, p->stream));
+  }
+  if (pre) CK(cudaStreamWaitEvent(p->stream, p->ev_pre, 0));
+  if (adj) CK(cudaStreamWaitEvent(p->stream, p->ev_adj, 0));
+  return NFFT_SUCCESS;
 }
 
 nfft_status copy_nodes(nfft_plan p, const void* nodes) {
@@ -674,6 +724,16 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     return fail(NFFT_ERROR_CUFFT);
   p->fft_ok = true;
   if (cufftSetStream(p->fft, p->stream) != CUFFT_SUCCESS) return fail(NFFT_ERROR_CUFFT);
+  if (cufftPlanMany(&p->fft_adj, D, n, nullptr, 1, 0, nullptr, 1, 0, c128 ? CUFFT_Z2Z : CUFFT_C2C, (int)p->B) !=
+      CUFFT_SUCCESS)
+    return fail(NFFT_ERROR_CUFFT);
+  p->fft_adj_ok = true;
+  if (cudaStreamCreateWithFlags(&p->side_pre, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&p->side_adj, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_pre, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_adj, cudaEventDisableTiming) != cudaSuccess)
+    return fail(NFFT_ERROR_CUDA);
 
   if (opt.timing) {
     for (auto& row : p->ev)
@@ -738,7 +798,7 @@ nfft_status nfft_set_nodes(nfft_plan p, const void* nodes) {
 nfft_status nfft_precompute(nfft_plan p) {
   if (!p) return NFFT_ERROR_INVALID_VALUE;
   DeviceGuard guard(p->device);
-  nfft_status s = p->prec == NFFT_COMPLEX128 ? precompute_impl<double>(p) : precompute_impl<float>(p);
+  nfft_status s = p->prec == NFFT_COMPLEX128 ? precompute_impl<double>(p, p->stream) : precompute_impl<float>(p, p->stream);
   if (s != NFFT_SUCCESS) return s;
   if (p->opt.check_nodes) {
     int err = 0;
@@ -773,7 +833,7 @@ nfft_status nfft_run_stage(nfft_plan p, int stage, const void* in, void* out) {
   if (!p || stage < NFFT_STAGE_PRECOMPUTE || stage > NFFT_STAGE_ADJ_CROP) return NFFT_ERROR_INVALID_VALUE;
   DeviceGuard guard(p->device);
   if (stage == NFFT_STAGE_PRECOMPUTE) {
-    nfft_status s = p->prec == NFFT_COMPLEX128 ? precompute_impl<double>(p) : precompute_impl<float>(p);
+    nfft_status s = p->prec == NFFT_COMPLEX128 ? precompute_impl<double>(p, p->stream) : precompute_impl<float>(p, p->stream);
     if (s == NFFT_SUCCESS) p->precomputed = true;
     return s;
   }
@@ -785,10 +845,28 @@ nfft_status nfft_run_stage(nfft_plan p, int stage, const void* in, void* out) {
   return p->prec == NFFT_COMPLEX128 ? run_stage_impl<double>(p, stage, in, out) : run_stage_impl<float>(p, stage, in, out);
 }
 
+nfft_status nfft_execute(nfft_plan p, int flags, const void* fhat_grid, void* f_nodes, const void* f_in,
+                         void* y_grid) {
+  if (!p || flags <= 0 || flags > 7) return NFFT_ERROR_INVALID_VALUE;
+  const bool fwd = flags & NFFT_EXEC_FORWARD, adj = flags & NFFT_EXEC_ADJOINT;
+  if (fwd && (!fhat_grid || !f_nodes || !is_device_pointer(fhat_grid) || !is_device_pointer(f_nodes)))
+    return NFFT_ERROR_INVALID_VALUE;
+  if (adj && (!f_in || !y_grid || !is_device_pointer(f_in) || !is_device_pointer(y_grid)))
+    return NFFT_ERROR_INVALID_VALUE;
+  if (!(flags & NFFT_EXEC_PRECOMPUTE) && !p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
+  DeviceGuard guard(p->device);
+  nfft_status s = p->prec == NFFT_COMPLEX128 ? execute_impl<double>(p, flags, fhat_grid, f_nodes, f_in, y_grid)
+                                             : execute_impl<float>(p, flags, fhat_grid, f_nodes, f_in, y_grid);
+  if (s == NFFT_SUCCESS && (flags & NFFT_EXEC_PRECOMPUTE)) p->precomputed = true;
+  return s;
+}
+
 nfft_status nfft_plan_destroy(nfft_plan p) {
   if (!p) return NFFT_ERROR_INVALID_VALUE;
   DeviceGuard guard(p->device);
   cudaError_t e = cudaStreamSynchronize(p->stream);
+  if (p->side_pre) cudaStreamSynchronize(p->side_pre);
+  if (p->side_adj) cudaStreamSynchronize(p->side_adj);
   free_all(p);
   delete p;
   if (e != cudaSuccess) {

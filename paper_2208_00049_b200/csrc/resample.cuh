@@ -247,6 +247,21 @@ __device__ __forceinline__ void scatter_tile(const Geom& g, typename cplx<T>::ty
 }
 
 // ------------------------------------------------------------ forward, tiled
+// Asynchronous global->shared copy of one grid cell (LDGSTS): the tile region
+// streams into shared memory while the threads load their nodes and evaluate
+// the taps, so the two memory latencies overlap.
+template <typename T>
+__device__ __forceinline__ void cp_async_cell(void* sdst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <typename T, int D, int M, int DEG>
 __global__ void __launch_bounds__(THREADS) interp_tiled_kernel(Geom g, WinPoly<T> wp,
                                                                const typename cplx<T>::type* __restrict__ grid,
@@ -265,15 +280,16 @@ __global__ void __launch_bounds__(THREADS) interp_tiled_kernel(Geom g, WinPoly<T
     T w[D][2 * M];
     int j = 0;
     bool has = threadIdx.x < sp.z;
-    if (has) {
-      const int i = sp.y + threadIdx.x;
-      j = perm[i];
-      has = node_setup<T, D, M, DEG>(g, wp, ks, i, tc, loc, w);
-    }
     for (int b = 0; b < g.B; ++b) {
       const C* src = grid + (long long)b * g.grid_cells;
       __syncthreads();  // previous users of the tile are done
-      for_region<D>(g, tc, [&](int r, long long off) { tile[r] = src[off]; });
+      for_region<D>(g, tc, [&](int r, long long off) { cp_async_cell<T>(&tile[r], src + off); });
+      if (b == 0 && has) {
+        const int i = sp.y + threadIdx.x;
+        j = perm[i];
+        has = node_setup<T, D, M, DEG>(g, wp, ks, i, tc, loc, w);
+      }
+      cp_async_wait_all();
       __syncthreads();
       if (has) f[(long long)b * g.M + j] = gather_tile<T, D, M>(g, tile, loc, w);
     }
@@ -960,22 +976,41 @@ __global__ void __launch_bounds__(THREADS) spread_gather_kernel(Geom g, WinPoly<
     const int4 sp = subs[sidx];
     const TileCoords tc = tile_coords<D, M>(g, sp.x);
     for (int i = threadIdx.x; i <= tile_cells; i += blockDim.x) start[i] = 0;
-    __syncthreads();
-    // 1. cells + histogram (node t of the subproblem handled by thread t, looping)
-    for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
-      const int i = sp.y + t;
-      int lc = 0;
-      bool ok = true;
+    // 1. node t of the subproblem -> thread t (looping for S > blockDim): cell, taps, j and f of batch 0
+    //    stay in registers; the histogram counts the local cells
+    constexpr int PER = 1;  // S <= THREADS (plan invariant)
+    int lcs[PER], jj[PER];
+    int locs[PER][D];
+    T w[PER][D][TAPS];
+    C f0[PER];
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        double frac;
-        const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
-        const int loc = c - tc.p[d] * g.Q[d];
-        ok = ok && (unsigned)loc < (unsigned)g.Q[d];
-        lc = lc * g.Q[d] + (ok ? loc : 0);
+    for (int u = 0; u < PER; ++u) {
+      const int t = threadIdx.x + u * blockDim.x;
+      lcs[u] = -1;
+      if (t < sp.z) {
+        const int i = sp.y + t;
+        bool ok = true;
+        int lc = 0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          double frac;
+          const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
+          locs[u][d] = c - tc.p[d] * g.Q[d];
+          ok = ok && (unsigned)locs[u][d] < (unsigned)g.Q[d];
+          lc = lc * g.Q[d] + (ok ? locs[u][d] : 0);
+          window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w[u][d]);
+        }
+        if (ok) {
+          lcs[u] = lc;
+          jj[u] = perm[i];
+          f0[u] = f[jj[u]];
+        }
       }
-      if (ok) atomicAdd(&start[lc + 1], 1);
     }
+    __syncthreads();  // start[] zeroed
+#pragma unroll
+    for (int u = 0; u < PER; ++u)
+      if (lcs[u] >= 0) atomicAdd(&start[lcs[u] + 1], 1);
     __syncthreads();
     {
       const int per = (tile_cells + 1 + blockDim.x - 1) / blockDim.x;
@@ -991,37 +1026,29 @@ __global__ void __launch_bounds__(THREADS) spread_gather_kernel(Geom g, WinPoly<
       }
     }
     __syncthreads();
-    // 2. sorted slots: taps, cells, node index
-    for (int t = threadIdx.x; t < sp.z; t += blockDim.x) {
-      const int i = sp.y + t;
-      int loc[D], lc = 0;
-      bool ok = true;
-      T w[D][TAPS];
+    // 2. sorted slots
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      if (lcs[u] < 0) continue;
+      const int slot = atomicAdd(&cursor[lcs[u]], 1);
+      js[slot] = jj[u];
+      fv[slot] = f0[u];
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        double frac;
-        const int c = node_cell((double)ks[(long long)d * g.M + i], g.Ntd[d], g.Nt[d], frac);
-        loc[d] = c - tc.p[d] * g.Q[d];
-        ok = ok && (unsigned)loc[d] < (unsigned)g.Q[d];
-        lc = lc * g.Q[d] + (ok ? loc[d] : 0);
-        window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w[d]);
-      }
-      if (!ok) continue;
-      const int slot = atomicAdd(&cursor[lc], 1);
-      js[slot] = perm[i];
+        cl[d * S + slot] = locs[u][d];
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        cl[d * S + slot] = loc[d];
-#pragma unroll
-        for (int l = 0; l < TAPS; ++l) tap[(slot * D + d) * TAPS + l] = w[d][l];
+        for (int l = 0; l < TAPS; ++l) tap[(slot * D + d) * TAPS + l] = w[u][d][l];
       }
     }
     __syncthreads();
     const int nvalid = start[tile_cells];
     // 3. per batch vector: every region cell gathered by one thread, reduced into the grid
     for (int b = 0; b < g.B; ++b) {
-      for (int q = threadIdx.x; q < nvalid; q += blockDim.x) fv[q] = f[(long long)b * g.M + js[q]];
-      __syncthreads();
+      if (b > 0) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < nvalid; q += blockDim.x) fv[q] = f[(long long)b * g.M + js[q]];
+        __syncthreads();
+      }
       C* dst = grid + (long long)b * g.grid_cells;
       for_region<D>(g, tc, [&](int r, long long o) {
         C acc;
@@ -1059,8 +1086,8 @@ __global__ void __launch_bounds__(THREADS) spread_gather_kernel(Geom g, WinPoly<
         }
         if (acc.x != (T)0 || acc.y != (T)0) red_add<T>(dst + o, acc);
       });
-      __syncthreads();
     }
+    __syncthreads();
   }
 }
 

@@ -347,3 +347,37 @@ def test_repeated_calls_and_stage_api(method):
     np.testing.assert_array_equal(out_f.cpu().numpy()[0], got_f)
     assert rel_l2(out_y.cpu().numpy()[0], got_y) < 1e-15
     plan.close()
+
+
+@pytest.mark.parametrize("D", [1, 2, 3])
+def test_execute_overlapped_matches_oracle(D):
+    """nfft_execute (precompute || forward deconv+FFT, adjoint || forward on
+    internal streams, joined into the plan stream) against the oracle, also
+    when captured into a CUDA graph and replayed."""
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    N = {1: (512,), 2: (40, 48), 3: (12, 10, 16)}[D]
+    w = workloads.make({1: "cfg2_1d_2e18", 2: "cfg3_2d_512", 3: "cfg4_3d_64"}[D], seed=16, N=N, M=2000, m=4)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        plan = pkg.NfftPlan(torch.from_numpy(w["nodes"]).cuda(), N, m=4, stream=st.cuda_stream)
+        fhat = torch.from_numpy(w["fhat"]).cuda()
+        f = torch.from_numpy(w["f"]).cuda()
+        fo = torch.empty((1, w["M"]), dtype=torch.complex128, device="cuda")
+        yo = torch.empty((1,) + N, dtype=torch.complex128, device="cuda")
+        plan.execute(True, fhat, fo, f, yo)
+    st.synchronize()
+    rf, ry = _oracle(w)
+    assert rel_l2(fo.cpu().numpy()[0], rf[0]) <= 1e-12
+    assert rel_l2(yo.cpu().numpy()[0], ry[0]) <= 1e-12
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        plan.execute(True, fhat, fo, f, yo)
+    fo.zero_()
+    yo.zero_()
+    with torch.cuda.stream(st):
+        g.replay()
+    st.synchronize()
+    assert rel_l2(fo.cpu().numpy()[0], rf[0]) <= 1e-12
+    assert rel_l2(yo.cpu().numpy()[0], ry[0]) <= 1e-12
+    plan.close()

@@ -17,7 +17,7 @@ import paper_2208_00049_b200 as pkg
 from paper_2208_00049_b200 import workloads
 
 
-def run(config, m, method="auto", tile=None, steps=20, flush=True, **over):
+def run(config, m, method="auto", tile=None, steps=20, flush=True, max_subproblem=0, **over):
     w = workloads.make(config, seed=0, m=m, **over)
     dev = torch.device("cuda", 0)
     st = torch.cuda.Stream()
@@ -26,11 +26,14 @@ def run(config, m, method="auto", tile=None, steps=20, flush=True, **over):
         fhat = torch.from_numpy(w["fhat"]).to(dev)
         f = torch.from_numpy(w["f"]).to(dev)
         p = pkg.NfftPlan(nodes, w["N"], m=m, sigma=w["sigma"], precision=w["precision"], batch=w["batch"],
-                         tile=tile, stream=st.cuda_stream, method=method, check_nodes=False)
+                         tile=tile, stream=st.cuda_stream, method=method, check_nodes=False,
+                         max_subproblem=max_subproblem)
         fo = torch.empty((w["batch"], w["M"]), dtype=p.tdtype_c, device=dev)
         yo = torch.empty((w["batch"],) + tuple(w["N"]), dtype=p.tdtype_c, device=dev)
-        buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-        rbuf = torch.ones(64 << 20, dtype=torch.float32, device=dev)
+        wmb = int(os.environ.get("FLUSH_WRITE_MB", "256"))
+        rmb = int(os.environ.get("FLUSH_READ_MB", "256"))
+        buf = torch.empty(max(wmb, 1) << 20, dtype=torch.uint8, device=dev)
+        rbuf = torch.ones(max(rmb, 4) << 18, dtype=torch.float32, device=dev)
         sink = torch.empty((), dtype=torch.float32, device=dev)
     stages = [("pre", lambda: p.run_stage("precompute")), ("deconv", lambda: p.run_stage("fwd_deconv", fhat)),
               ("fftF", lambda: p.run_stage("fwd_fft")), ("interp", lambda: p.run_stage("fwd_interp", None, fo)),
@@ -52,8 +55,10 @@ def run(config, m, method="auto", tile=None, steps=20, flush=True, **over):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(graphs) + 1)]
         with torch.cuda.stream(st):
             if flush:
-                buf.zero_()
-                sink.copy_(rbuf.sum())
+                if wmb > 0:
+                    buf.zero_()
+                if rmb > 0:
+                    sink.copy_(rbuf.sum())
             for k, (_, g) in enumerate(graphs):
                 ev[k].record(st)
                 g.replay()
@@ -70,6 +75,14 @@ def run(config, m, method="auto", tile=None, steps=20, flush=True, **over):
 
 if __name__ == "__main__":
     cases = []
+    if len(sys.argv) > 1 and sys.argv[1] == "sweep":
+        for cfg, tiles in (("cfg2_1d_2e18", [(128,), (256,), (512,), (1024,), (2048,)]),
+                           ("cfg3_2d_512", [(16, 16), (16, 32), (32, 32), (32, 64), (64, 64)])):
+            for t in tiles:
+                for S in (128, 256):
+                    r, info = run(cfg, 4, "tiled", t, max_subproblem=S)
+                    print(json.dumps({"cfg": cfg, "tile": t, "S": S, "us": r}), flush=True)
+        sys.exit(0)
     if len(sys.argv) > 1:
         tile = tuple(int(x) for x in sys.argv[4].split(",")) if len(sys.argv) > 4 else None
         cases = [(sys.argv[1], int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else "auto", tile)]
