@@ -72,7 +72,10 @@ typedef enum {
   NFFT_METHOD_TILED_CAS = 3, /* tiled; adjoint accumulates with shared-memory atomics (reference variant) */
   NFFT_METHOD_TILED_LOC = 4, /* tiled; adjoint lanes-own-cells + global reduction flush (D <= 2) */
   NFFT_METHOD_TILED_OWN = 5, /* tiled; adjoint owner-computes, no atomics, no zero pass (D <= 2) */
-  NFFT_METHOD_TILED_SORTED = 6 /* tiled; adjoint thread-per-node over cell-sorted warp chunks */
+  NFFT_METHOD_TILED_SORTED = 6, /* tiled; adjoint thread-per-node over cell-sorted warp chunks */
+  NFFT_METHOD_TILED_V1 = 7 /* first-generation path: three-kernel sort + subproblem-list tiled kernels
+                              (AUTO/TILED use the cooperative one-kernel sort and, for D = 1, the
+                              static-tile interp / owner-computes spread when Q | Ntilde, P >= 3, Q >= 2m) */
 } nfft_method;
 
 typedef struct {

@@ -36,7 +36,7 @@ STATUS = {
     3: "NFFT_ERROR_NONFINITE_NODE", 4: "NFFT_ERROR_BAD_TILE", 5: "NFFT_ERROR_NOT_PRECOMPUTED",
     6: "NFFT_ERROR_OUT_OF_MEMORY", 7: "NFFT_ERROR_CUDA", 8: "NFFT_ERROR_CUFFT", 9: "NFFT_ERROR_UNSUPPORTED",
 }
-METHODS = {"auto": 0, "tiled": 1, "direct": 2, "tiled_cas": 3, "tiled_loc": 4, "tiled_own": 5, "tiled_sorted": 6}
+METHODS = {"auto": 0, "tiled": 1, "direct": 2, "tiled_cas": 3, "tiled_loc": 4, "tiled_own": 5, "tiled_sorted": 6, "tiled_v1": 7}
 PRECISIONS = {"c64": 0, "c128": 1}
 
 

@@ -19,6 +19,9 @@ struct KernelSet {
   int own_threads;
   void (*spread_sorted)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
   void (*spread_gather)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
+  // D = 1 static-tile kernels (resample1d.cuh)
+  void (*interp1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
+  void (*spread1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
 };
 
 template <typename T> KernelSet<T> kernels_d1(int m);
@@ -36,13 +39,18 @@ inline KernelSet<T> kernels_for(int D, int m) {
 
 #ifdef NFFTB_INSTANTIATE_D
 #include "resample.cuh"
+#include "resample1d.cuh"
 namespace nfftb {
 template <typename T, int D, int M>
 KernelSet<T> make_set() {
   constexpr int DEG = poly_degree(M, sizeof(T) == 8);
   KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
                  interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
-                 spread_sorted_kernel<T, D, M, DEG>, nullptr};
+                 spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr};
+  if constexpr (D == 1) {
+    k.interp1 = interp1d_kernel<T, M, DEG>;
+    k.spread1 = spread1d_kernel<T, M, DEG>;
+  }
   if constexpr (D <= 2) {
     k.spread_loc = spread_loc_kernel<T, D, M, DEG>;
     k.loc_threads = LocCfg<T, D, M>::THR;

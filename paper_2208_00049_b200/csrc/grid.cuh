@@ -112,4 +112,42 @@ __global__ void __launch_bounds__(THREADS) crop_zero_kernel(Geom g, typename cpl
   }
 }
 
+// Alg. 2 lines 7-9 without the re-zeroing, for spreading kernels that write
+// every grid cell themselves (resample1d.cuh: owner-computes): one thread per
+// N-grid cell, rows as in deconv_place_kernel.
+template <typename T>
+__global__ void __launch_bounds__(THREADS) crop_kernel(Geom g, const typename cplx<T>::type* __restrict__ grid,
+                                                       const T* __restrict__ beta,
+                                                       typename cplx<T>::type* __restrict__ y) {
+  using C = typename cplx<T>::type;
+  const int D = g.D;
+  const int ntl = g.Nt[D - 1], nl = g.N[D - 1];
+  const long long rows = (long long)g.B * (g.ngrid_cells / nl);
+  for (long long row = blockIdx.y; row < rows; row += gridDim.y) {
+    int i[MAX_D];
+    const int b = decode_row(row, D, g.N, i);
+    T scale = (T)1;
+    long long lin = 0;
+    for (int d = 0; d < D - 1; ++d) {
+      const int n = i[d] - (g.N[d] >> 1);
+      const int s = n < 0 ? n + g.Nt[d] : n;
+      scale *= beta[g.beta_off[d] + i[d]];
+      lin = lin * g.Nt[d] + s;
+    }
+    const C* src = grid + (long long)b * g.grid_cells + lin * ntl;
+    C* dst = y + row * nl;
+    const T* bl = beta + g.beta_off[D - 1];
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nl; x += gridDim.x * blockDim.x) {
+      const int n = x - (nl >> 1);
+      const int s = n < 0 ? n + ntl : n;
+      const C v = src[s];
+      const T sc = scale * bl[x];
+      C out;
+      out.x = v.x * sc;
+      out.y = v.y * sc;
+      dst[x] = out;
+    }
+  }
+}
+
 }  // namespace nfftb

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -20,6 +21,8 @@
 #include "dispatch.cuh"
 #include "grid.cuh"
 #include "precompute.cuh"
+#include "binsort.cuh"
+#include "resample1d.cuh"
 
 using namespace nfftb;
 
@@ -73,6 +76,11 @@ struct nfft_plan_s {
   int* d_tile_total = nullptr; // n_tiles
   unsigned* d_ticket = nullptr;
   int cs_nblk = 1;
+  bool use_bs = false;    // one cooperative binsort kernel (binsort.cuh) instead of cs_count/scan/scatter
+  int bs_grid = 0, bs_rr = 1;
+  size_t bs_bytes = 0;
+  bool use_r1 = false;    // D = 1 static-tile interp / owner-computes spread (resample1d.cuh)
+  size_t r1_interp_bytes = 0, r1_spread_bytes = 0;
   void* d_grid_in = nullptr;  // B * prod Nt complex: forward input, zero padding persists
   void* d_grid = nullptr;     // B * prod Nt complex: forward FFT output (read by interp)
   void* d_grid_adj = nullptr; // B * prod Nt complex: adjoint grid, all zero between adjoints
@@ -213,7 +221,7 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
     p->grid_tiled = (int)std::max<int64_t>(1, std::min<int64_t>(p->max_subs, (int64_t)occ_min * p->sm_count));
     p->grid_gather = 0;
-    if (ks.spread_gather && p->opt.method <= NFFT_METHOD_TILED) {
+    if (ks.spread_gather && (p->opt.method <= NFFT_METHOD_TILED || p->opt.method == NFFT_METHOD_TILED_V1)) {
       int tile_cells = 1;
       for (int d = 0; d < p->D; ++d) tile_cells *= (int)p->Q[d];
       const size_t bytes = gather_smem_bytes(p->D, p->m, p->csize(), p->rsize(), tile_cells, p->S);
@@ -230,7 +238,8 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
       cudaGetLastError();
     }
     p->grid_sorted = 0;
-    if (p->opt.method == NFFT_METHOD_TILED_SORTED || (p->opt.method <= NFFT_METHOD_TILED && p->D == 3)) {
+    if (p->opt.method == NFFT_METHOD_TILED_SORTED ||
+        ((p->opt.method <= NFFT_METHOD_TILED || p->opt.method == NFFT_METHOD_TILED_V1) && p->D == 3)) {
       int tile_cells = 1;
       for (int d = 0; d < p->D; ++d) tile_cells *= (int)p->Q[d];
       const size_t bytes = p->region_bytes + (size_t)(tile_cells + 1 + THREADS + 17) * 4;
@@ -287,7 +296,108 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
   }
   p->grid_direct = p->sm_count * 8;
+  p->use_r1 = false;
+  if (p->D == 1 && ks.interp1 && (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED) &&
+      p->Nt[0] % p->Q[0] == 0 && p->P[0] >= 3 && p->Q[0] >= 2 * p->m) {
+    const size_t ib = (size_t)r1_region_cells((int)p->Q[0], p->m, p->prec == NFFT_COMPLEX128) * p->csize();
+    const size_t sb = r1_spread_smem_bytes((int)p->Q[0], p->m, p->csize(), p->rsize());
+    int occ_i = 0, occ_s = 0;
+    if (ib <= 227 * 1024 && sb <= 227 * 1024 &&
+        cudaFuncSetAttribute((const void*)ks.interp1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib) == cudaSuccess &&
+        cudaFuncSetAttribute((const void*)ks.spread1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp1, R1_THREADS, ib) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, R1_THREADS, sb) == cudaSuccess &&
+        occ_i >= 1 && occ_s >= 1) {
+      p->use_r1 = true;
+      p->r1_interp_bytes = ib;
+      p->r1_spread_bytes = sb;
+    }
+    cudaGetLastError();
+  }
   return NFFT_SUCCESS;
+}
+
+#define TRY(x)                          \
+  do {                                  \
+    nfft_status s_ = (x);               \
+    if (s_ != NFFT_SUCCESS) return s_;  \
+  } while (0)
+
+template <typename R, int RR>
+void* binsort_fn(int D) {
+  if (D == 1) return (void*)binsort_kernel<R, RR, 1>;
+  if (D == 2) return (void*)binsort_kernel<R, RR, 2>;
+  return (void*)binsort_kernel<R, RR, 3>;
+}
+template <typename R>
+void* binsort_fn_rr(int rr, int D) {
+  switch (rr) {
+    case 1: return binsort_fn<R, 1>(D);
+    case 2: return binsort_fn<R, 2>(D);
+    case 4: return binsort_fn<R, 4>(D);
+    default: return binsort_fn<R, 8>(D);
+  }
+}
+
+// Cooperative launch (all CTAs co-resident: the kernel synchronises the grid).
+template <typename R>
+nfft_status launch_binsort(nfft_plan p, cudaStream_t st) {
+  const R* nodes = (const R*)p->d_nodes;
+  Geom g = p->geom;
+  int P = (int)p->n_tiles;
+  int nb = p->node_begin, ne = p->node_end, S = p->S;
+  R* ks = (R*)p->d_ks;
+  void* args[] = {(void*)&nodes, (void*)&g, (void*)&P, (void*)&p->d_cnt, (void*)&p->d_tile_total,
+                  (void*)&p->d_offsets, (void*)&p->d_perm, (void*)&ks, (void*)&p->d_err, (void*)&nb, (void*)&ne,
+                  (void*)&S, (void*)&p->d_subbase, (void*)&p->d_subs};
+  CK(cudaLaunchCooperativeKernel(binsort_fn_rr<R>(p->bs_rr, p->D), dim3(p->bs_grid), dim3(BS_THREADS), args, p->bs_bytes, st));
+  ++p->launches;
+  return NFFT_SUCCESS;
+}
+
+// Chooses the cooperative single-kernel sort when every CTA fits on the GPU at
+// once with <= 8 rounds of 512 nodes and the per-warp tile counters fit shared memory.
+template <typename R>
+void configure_binsort(nfft_plan p) {
+  p->use_bs = false;
+  const int P = (int)p->n_tiles;
+  const size_t bytes = binsort_smem_bytes(P);
+  if (bytes > 200 * 1024) return;
+  // Each grid barrier costs about one same-address L2 atomic per CTA, so the
+  // smallest grid that still gives every SM one CTA wins (measured on B200,
+  // M = 2^18: 512 CTAs 68 us, 256 CTAs 37 us, 128 CTAs 25 us, 64 CTAs 32 us
+  // per precompute stage including the graph launch).
+  const char* env = getenv("NFFTB_BS_RR");  // diagnostics: force one rounds-per-warp value
+  int best_rr = 0, best_g = 0, best_over = 1 << 30;
+  for (int rr : {1, 2, 4, 8}) {
+    if (env && rr != atoi(env)) continue;
+    void* fn = binsort_fn_rr<R>(rr, p->D);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BS_THREADS, bytes) != cudaSuccess || occ < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    const int64_t E = (int64_t)BS_THREADS * rr;
+    const int64_t G = (p->M + E - 1) / E;
+    if (G > (int64_t)occ * p->sm_count || G > p->cs_nblk) continue;
+    // distance from one CTA per SM (fewer CTAs preferred when equal)
+    const int over = G <= p->sm_count ? (int)(p->sm_count - G) : (int)(G - p->sm_count) * 2;
+    if (over < best_over) {
+      best_over = over;
+      best_rr = rr;
+      best_g = (int)G;
+    }
+  }
+  if (best_rr > 0) {
+    p->use_bs = true;
+    p->bs_grid = best_g;
+    p->bs_rr = best_rr;
+    p->bs_bytes = bytes;
+  }
 }
 
 template <typename R>
@@ -296,6 +406,11 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
   const int nt = (int)p->n_tiles;
   CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), st));
   rec(p, 2, 0);
+  if (p->use_bs) {
+    TRY(launch_binsort<R>(p, st));
+    rec(p, 2, 1);
+    return NFFT_SUCCESS;
+  }
   // stable counting sort into tiles: count, scan (+ offsets, subproblems), scatter (precompute.cuh)
   cs_count_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, st>>>((const R*)p->d_nodes, p->geom, nt,
                                                                            p->d_cnt, p->d_err);
@@ -353,7 +468,10 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   const auto* grid = (const typename cplx<T>::type*)p->d_grid;
-  if (p->tiled) {
+  if (p->use_r1) {
+    ks.interp1<<<(unsigned)p->n_tiles, R1_THREADS, p->r1_interp_bytes, st>>>(
+        p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
+  } else if (p->tiled) {
     ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
   } else {
@@ -370,6 +488,15 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   auto* grid = (typename cplx<T>::type*)p->d_grid_adj;  // all zero on entry (plan creation / previous crop)
+  if (p->use_r1) {
+    // owner-computes: every grid cell written exactly once, no zero pass
+    rec(p, 1, 1);
+    ks.spread1<<<(unsigned)p->n_tiles, R1_THREADS, p->r1_spread_bytes, st>>>(
+        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, grid);
+    ++p->launches;
+    CKL();
+    return NFFT_SUCCESS;
+  }
   if (p->tiled && p->grid_own > 0) {
     // owner-computes: every grid cell written exactly once, no zero pass
     rec(p, 1, 1);
@@ -404,6 +531,15 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
 template <typename T>
 nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st) {
   const Geom& g = p->geom;
+  if (p->use_r1) {  // the spread rewrites every cell: crop only, no re-zeroing
+    const int nl = g.N[g.D - 1];
+    const long long rows = (long long)g.B * (g.ngrid_cells / nl);
+    dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
+    crop_kernel<T><<<grid, THREADS, 0, st>>>(g, (const typename cplx<T>::type*)p->d_grid_adj, (const T*)p->d_betaT, y);
+    ++p->launches;
+    CKL();
+    return NFFT_SUCCESS;
+  }
   const int ntl = g.Nt[g.D - 1];
   const long long rows = (long long)g.B * (g.grid_cells / ntl);
   dim3 grid((unsigned)std::min<long long>((ntl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
@@ -413,12 +549,6 @@ nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st) 
   CKL();
   return NFFT_SUCCESS;
 }
-
-#define TRY(x)                          \
-  do {                                  \
-    nfft_status s_ = (x);               \
-    if (s_ != NFFT_SUCCESS) return s_;  \
-  } while (0)
 
 template <typename T>
 nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
@@ -553,7 +683,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   nfft_default_options(&opt);
   if (opt_in) opt = *opt_in;
   if (opt.batch < 1) return NFFT_ERROR_INVALID_VALUE;
-  if (opt.method < 0 || opt.method > 6) return NFFT_ERROR_INVALID_VALUE;
+  if (opt.method < 0 || opt.method > 7) return NFFT_ERROR_INVALID_VALUE;
   if (!(sigma > 1.0) || !std::isfinite(sigma)) return NFFT_ERROR_BAD_GEOMETRY;
   if (m > MAX_M) return NFFT_ERROR_UNSUPPORTED;
   if (M > (int64_t)0x7fffffff - 1) return NFFT_ERROR_UNSUPPORTED;
@@ -745,10 +875,12 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     p->k64 = kernels_for<double>(D, m);
     st = build_window_tables<double>(p);
     if (st == NFFT_SUCCESS) st = configure_kernels<double>(p, p->k64);
+    if (st == NFFT_SUCCESS && opt.method != NFFT_METHOD_TILED_V1) configure_binsort<double>(p);
   } else {
     p->k32 = kernels_for<float>(D, m);
     st = build_window_tables<float>(p);
     if (st == NFFT_SUCCESS) st = configure_kernels<float>(p, p->k32);
+    if (st == NFFT_SUCCESS && opt.method != NFFT_METHOD_TILED_V1) configure_binsort<float>(p);
   }
   if (st == NFFT_SUCCESS) st = copy_nodes(p, nodes);
   if (st == NFFT_SUCCESS) {

@@ -381,3 +381,57 @@ def test_execute_overlapped_matches_oracle(D):
     assert rel_l2(fo.cpu().numpy()[0], rf[0]) <= 1e-12
     assert rel_l2(yo.cpu().numpy()[0], ry[0]) <= 1e-12
     plan.close()
+
+
+# ------------------------------------------------------------------ D = 1 static-tile path + one-kernel sort
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("tile", [(64,), (128,)])
+def test_1d_static_tile_path(m, tile):
+    """Q | Ntilde, P >= 3, Q >= 2m selects interp1d / spread1d (owner-computes,
+    crop without re-zeroing) and the cooperative sort; batch 2, c128 + c64."""
+    w = workloads.make("cfg2_1d_2e18", seed=21, N=(256,), M=900, m=m, batch=2)
+    _check(w, tile=tile)
+    w32 = dict(w, nodes=w["nodes"].astype(np.float32), fhat=w["fhat"].astype(np.complex64),
+               f=w["f"].astype(np.complex64), precision="c64")
+    _check(w32, tile=tile)
+
+
+def test_1d_static_tile_overfull_tile_and_shards():
+    """Clustered nodes: one tile holds > 512 candidates (several spread
+    chunks, read-modify-write of owned cells); wrap-around at both ends;
+    node shards of the sorted order sum to the full adjoint."""
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    from paper_2208_00049_b200 import dist
+    rng = np.random.default_rng(22)
+    nodes = np.concatenate([rng.random(1500) * 0.05, rng.random(500) - 0.5,
+                            [-0.5, 0.5 - 1e-9, 0.4999, -0.4999, 0.0]])[:, None]
+    M = nodes.shape[0]
+    w = dict(nodes=nodes, N=(256,), m=4, sigma=2.0, precision="c128", batch=1,
+             fhat=workloads.complex_normal(rng, (1, 256)), f=workloads.complex_normal(rng, (1, M)))
+    full_f, full_y, _ = _run(w, tile=(32,))
+    rf, ry = _oracle(w)
+    assert rel_l2(full_f[0], rf[0]) <= 1e-12 and rel_l2(full_y[0], ry[0]) <= 1e-12
+    acc = np.zeros_like(full_y)
+    for rank in range(3):
+        rg = dist.shard_range(M, rank, 3)
+        plan = pkg.NfftPlan(torch.from_numpy(nodes).cuda(), (256,), m=4, tile=(32,), node_range=rg).precompute()
+        acc += plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
+        plan.close()
+    assert rel_l2(acc, full_y) < 1e-14
+
+
+@pytest.mark.parametrize("config", ["cfg2_1d_2e18", "cfg3_2d_512", "cfg4_3d_64", "cfg5_radial_s2"])
+def test_one_kernel_sort_matches_three_kernel_sort(config):
+    """The cooperative binsort (default) and the first-generation three-kernel
+    sort (method tiled_v1) give the identical permutation and offsets."""
+    w = workloads.make(config, seed=4, batch=1)
+    a = _plan(w)
+    b = _plan(w, method="tiled_v1")
+    pa, oa = a.binning()
+    pb, ob = b.binning()
+    a.close()
+    b.close()
+    np.testing.assert_array_equal(pa, pb)
+    np.testing.assert_array_equal(oa, ob)
