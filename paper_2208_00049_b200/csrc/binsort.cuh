@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(BS_THREADS) binsort_kernel(const R* __restrict
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char bs_smem[];
-  unsigned short* wc = reinterpret_cast<unsigned short*>(bs_smem);                         // [16][P]
+  unsigned short* wc = reinterpret_cast<unsigned short*>(bs_smem);  // [P][16]: per tile, one u16 counter per warp
   int* offs = reinterpret_cast<int*>(bs_smem + (((size_t)BS_WARPS * P * 2 + 15) & ~(size_t)15));  // [P+1]
   __shared__ int ws[32];
   __shared__ int psum[BS_THREADS];
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(BS_THREADS) binsort_kernel(const R* __restrict
   int key[RR], rank[RR];
   R kc[RR][MAX_D];
   bool any_bad = false;
-  unsigned short* mine = wc + warp * P;
+  unsigned short* mine = wc + warp;  // counter of tile t for this warp: mine[16 t]
 #pragma unroll
   for (int r = 0; r < RR; ++r) {
     const int j = base + (warp * RR + r) * 32 + lane;
@@ -100,28 +100,34 @@ __global__ void __launch_bounds__(BS_THREADS) binsort_kernel(const R* __restrict
       any_bad |= bad;
     }
     const unsigned peers = __match_any_sync(0xffffffffu, key[r]);
-    rank[r] = key[r] >= 0 ? (int)mine[key[r]] + __popc(peers & lt) : 0;
+    rank[r] = key[r] >= 0 ? (int)mine[key[r] * BS_WARPS] + __popc(peers & lt) : 0;
     __syncwarp();
-    if (key[r] >= 0 && lane == __ffs(peers) - 1) mine[key[r]] = (unsigned short)(mine[key[r]] + __popc(peers));
+    if (key[r] >= 0 && lane == __ffs(peers) - 1)
+      mine[key[r] * BS_WARPS] = (unsigned short)(mine[key[r] * BS_WARPS] + __popc(peers));
     __syncwarp();
   }
   if (any_bad) atomicOr(err, 1);
   __syncthreads();
   int* crow = cnt + (long long)b * P;
-  for (int t = tid; t < P; t += BS_THREADS) {
-    int run = 0;
+  for (int t = tid; t < P; t += BS_THREADS) {  // exclusive prefix over the 16 warps: 32 bytes per tile
+    uint4* row = reinterpret_cast<uint4*>(wc + t * BS_WARPS);
+    uint4 v[2] = {row[0], row[1]};
+    unsigned* u = reinterpret_cast<unsigned*>(v);
+    unsigned run = 0;
 #pragma unroll
-    for (int w = 0; w < BS_WARPS; ++w) {
-      const int c = wc[w * P + t];
-      wc[w * P + t] = (unsigned short)run;
-      run += c;
+    for (int k = 0; k < 8; ++k) {
+      const unsigned lo = u[k] & 0xffffu, hi = u[k] >> 16;
+      u[k] = run | ((run + lo) << 16);
+      run += lo + hi;
     }
-    crow[t] = run;
+    row[0] = v[0];
+    row[1] = v[1];
+    crow[t] = (int)run;
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < RR; ++r)
-    if (key[r] >= 0) rank[r] += mine[key[r]];
+    if (key[r] >= 0) rank[r] += mine[key[r] * BS_WARPS];
   grid.sync();
 
   // ---------------- phase 2: column prefix of cnt over the G CTA rows

@@ -53,10 +53,19 @@ __device__ __forceinline__ int node_cell(double k, double Ntd, int Nt, double& f
   const double t = __dmul_rn(Ntd, k);
   const double a = floor(t);
   frac = t - a;
-  const double r = fmod(a, Ntd);  // exact for integer-valued doubles, |r| < Ntilde
-  int c = (int)r + (Nt >> 1);
-  if (c < 0) c += Nt;
-  else if (c >= Nt) c -= Nt;
+  int c;
+  if (fabs(a) < 1073741824.0) {  // |a| < 2^30: exact as int; c = (a + Nt/2) mod Nt, usually no wrap
+    c = (int)a + (Nt >> 1);
+    if ((unsigned)c >= (unsigned)Nt) {
+      c %= Nt;
+      if (c < 0) c += Nt;
+    }
+  } else {  // nodes far outside the torus (periodic fold, reading R10)
+    const double r = fmod(a, Ntd);  // exact for integer-valued doubles, |r| < Ntilde
+    c = (int)r + (Nt >> 1);
+    if (c < 0) c += Nt;
+    else if (c >= Nt) c -= Nt;
+  }
   return c;
 }
 
@@ -116,6 +125,19 @@ __host__ __device__ inline size_t gather_smem_bytes(int D, int M, size_t csize, 
   b += (size_t)S * 4 * (D + 1);              // local cell per dim, node j
   b += (size_t)2 * (tile_cells + 1) * 4;     // cell offsets, cursors
   return b;
+}
+
+// ---- warp-wide exclusive scan of one int per lane ----
+__device__ __forceinline__ int warp_exclusive_scan(int x, int& total) {
+  const int lane = threadIdx.x & 31;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  total = __shfl_sync(0xffffffffu, inc, 31);
+  return inc - x;
 }
 
 // ---- block-wide exclusive scan of one int per thread (blockDim = THREADS) ----

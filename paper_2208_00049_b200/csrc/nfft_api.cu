@@ -23,6 +23,7 @@
 #include "precompute.cuh"
 #include "binsort.cuh"
 #include "resample1d.cuh"
+#include "resample_nd.cuh"
 
 using namespace nfftb;
 
@@ -80,6 +81,7 @@ struct nfft_plan_s {
   int bs_grid = 0, bs_rr = 1;
   size_t bs_bytes = 0;
   bool use_r1 = false;    // D = 1 static-tile interp / owner-computes spread (resample1d.cuh)
+  bool use_ind = false;   // D = 2, 3 static-tile interpolation (resample_nd.cuh)
   size_t r1_interp_bytes = 0, r1_spread_bytes = 0;
   void* d_grid_in = nullptr;  // B * prod Nt complex: forward input, zero padding persists
   void* d_grid = nullptr;     // B * prod Nt complex: forward FFT output (read by interp)
@@ -299,19 +301,31 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
   p->use_r1 = false;
   if (p->D == 1 && ks.interp1 && (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED) &&
       p->Nt[0] % p->Q[0] == 0 && p->P[0] >= 3 && p->Q[0] >= 2 * p->m) {
-    const size_t ib = (size_t)r1_region_cells((int)p->Q[0], p->m, p->prec == NFFT_COMPLEX128) * p->csize();
-    const size_t sb = r1_spread_smem_bytes((int)p->Q[0], p->m, p->csize(), p->rsize());
+    const size_t ib = (size_t)W1_WARPS * (((size_t)r1_region_cells((int)p->Q[0], p->m, p->prec == NFFT_COMPLEX128) + 7) & ~(size_t)7) * p->csize();
+    const size_t sb = (size_t)W1_WARPS * r1_spread_warp_bytes((int)p->Q[0], p->m, p->csize(), p->rsize());
     int occ_i = 0, occ_s = 0;
     if (ib <= 227 * 1024 && sb <= 227 * 1024 &&
         cudaFuncSetAttribute((const void*)ks.interp1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib) == cudaSuccess &&
         cudaFuncSetAttribute((const void*)ks.spread1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp1, R1_THREADS, ib) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, R1_THREADS, sb) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp1, W1_THREADS, ib) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, W1_THREADS, sb) == cudaSuccess &&
         occ_i >= 1 && occ_s >= 1) {
       p->use_r1 = true;
       p->r1_interp_bytes = ib;
       p->r1_spread_bytes = sb;
     }
+    cudaGetLastError();
+  }
+  p->use_ind = false;
+  if (p->D >= 2 && p->tiled && ks.interp_nd &&
+      (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED)) {
+    int occ = 0;
+    if (cudaFuncSetAttribute((const void*)ks.interp_nd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)p->region_bytes) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ks.interp_nd, RN_THREADS, p->region_bytes) ==
+            cudaSuccess &&
+        occ >= 1)
+      p->use_ind = true;
     cudaGetLastError();
   }
   return NFFT_SUCCESS;
@@ -468,8 +482,11 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   const auto* grid = (const typename cplx<T>::type*)p->d_grid;
-  if (p->use_r1) {
-    ks.interp1<<<(unsigned)p->n_tiles, R1_THREADS, p->r1_interp_bytes, st>>>(
+  if (p->use_ind) {
+    ks.interp_nd<<<(unsigned)p->n_tiles, RN_THREADS, p->region_bytes, st>>>(
+        p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
+  } else if (p->use_r1) {
+    ks.interp1<<<(unsigned)((p->n_tiles + W1_WARPS - 1) / W1_WARPS), W1_THREADS, p->r1_interp_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
   } else if (p->tiled) {
     ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
@@ -491,7 +508,7 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   if (p->use_r1) {
     // owner-computes: every grid cell written exactly once, no zero pass
     rec(p, 1, 1);
-    ks.spread1<<<(unsigned)p->n_tiles, R1_THREADS, p->r1_spread_bytes, st>>>(
+    ks.spread1<<<(unsigned)((p->n_tiles + W1_WARPS - 1) / W1_WARPS), W1_THREADS, p->r1_spread_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, grid);
     ++p->launches;
     CKL();
@@ -708,7 +725,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   for (int d = 0; d < D; ++d) {
     int64_t q = opt.tile[d];
     if (q < 0 || q > Nt[d]) return NFFT_ERROR_BAD_TILE;
-    if (q == 0) q = D == 1 ? 512 : (D == 2 ? 32 : 8);
+    if (q == 0) q = D == 1 ? 128 : (D == 2 ? 32 : 8);
     q = std::min<int64_t>(q, Nt[d]);
     Q[d] = q;
     P[d] = (Nt[d] + q - 1) / q;
