@@ -20,8 +20,8 @@ struct KernelSet {
   void (*spread_sorted)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
   void (*spread_gather)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
   // D = 1 static-tile kernels (resample1d.cuh)
-  void (*interp1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
-  void (*spread1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
+  void (*interp1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
+  void (*spread1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, const int*, int, int, int, C*);
   // D = 2, 3 static-tile interpolation (resample_nd.cuh)
   void (*interp_nd)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
 };
@@ -51,8 +51,8 @@ KernelSet<T> make_set() {
                  interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
                  spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr};
   if constexpr (D == 1) {
-    k.interp1 = interp1d_kernel<T, M, DEG>;
-    k.spread1 = spread1d_kernel<T, M, DEG>;
+    k.interp1 = interp1c_kernel<T, M, DEG>;
+    k.spread1 = spread1c_kernel<T, M, DEG>;
   } else {
     k.interp_nd = interp_nd_kernel<T, D, M, DEG>;
   }

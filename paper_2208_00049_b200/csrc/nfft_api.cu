@@ -22,6 +22,7 @@
 #include "grid.cuh"
 #include "precompute.cuh"
 #include "binsort.cuh"
+#include "cellsort.cuh"
 #include "resample1d.cuh"
 #include "resample_nd.cuh"
 
@@ -80,9 +81,13 @@ struct nfft_plan_s {
   bool use_bs = false;    // one cooperative binsort kernel (binsort.cuh) instead of cs_count/scan/scatter
   int bs_grid = 0, bs_rr = 1;
   size_t bs_bytes = 0;
-  bool use_r1 = false;    // D = 1 static-tile interp / owner-computes spread (resample1d.cuh)
+  bool use_r1 = false;    // D = 1 cell-sorted interp / owner-computes spread (resample1d.cuh)
   bool use_ind = false;   // D = 2, 3 static-tile interpolation (resample_nd.cuh)
-  size_t r1_interp_bytes = 0, r1_spread_bytes = 0;
+  size_t r1_sort_bytes = 0, r1_spread_bytes = 0;
+  void* d_kc = nullptr;     // M reals: coordinates in cell order (D = 1)
+  int* d_jc = nullptr;      // M: node index of every cell-sorted position
+  int* d_ic = nullptr;      // M: tile-sorted position of every cell-sorted position (shards)
+  int* d_cstart = nullptr;  // Ntilde + 1: first cell-sorted position of every cell
   void* d_grid_in = nullptr;  // B * prod Nt complex: forward input, zero padding persists
   void* d_grid = nullptr;     // B * prod Nt complex: forward FFT output (read by interp)
   void* d_grid_adj = nullptr; // B * prod Nt complex: adjoint grid, all zero between adjoints
@@ -155,7 +160,7 @@ bool is_device_pointer(const void* p) {
 void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
-                  p->d_ticket, p->d_perm};
+                  p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_ic, p->d_cstart};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -299,19 +304,19 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
   }
   p->grid_direct = p->sm_count * 8;
   p->use_r1 = false;
-  if (p->D == 1 && ks.interp1 && (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED) &&
-      p->Nt[0] % p->Q[0] == 0 && p->P[0] >= 3 && p->Q[0] >= 2 * p->m) {
-    const size_t ib = (size_t)W1_WARPS * (((size_t)r1_region_cells((int)p->Q[0], p->m, p->prec == NFFT_COMPLEX128) + 7) & ~(size_t)7) * p->csize();
-    const size_t sb = (size_t)W1_WARPS * r1_spread_warp_bytes((int)p->Q[0], p->m, p->csize(), p->rsize());
-    int occ_i = 0, occ_s = 0;
-    if (ib <= 227 * 1024 && sb <= 227 * 1024 &&
-        cudaFuncSetAttribute((const void*)ks.interp1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib) == cudaSuccess &&
+  if (p->D == 1 && ks.interp1 && (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED)) {
+    const size_t cb = cst_smem_bytes((int)p->Q[0]);
+    const size_t sb = (size_t)S1_WARPS * s1_warp_bytes(p->m, p->csize(), p->rsize());
+    const void* csfn = p->prec == NFFT_COMPLEX128 ? (const void*)cellsort_kernel<double, 1> : (const void*)cellsort_kernel<float, 1>;
+    int occ_c = 0, occ_s = 0;
+    if (cb <= 200 * 1024 &&
+        cudaFuncSetAttribute(csfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb) == cudaSuccess &&
         cudaFuncSetAttribute((const void*)ks.spread1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp1, W1_THREADS, ib) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, W1_THREADS, sb) == cudaSuccess &&
-        occ_i >= 1 && occ_s >= 1) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, csfn, CST_THREADS, cb) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, 32 * S1_WARPS, sb) == cudaSuccess &&
+        occ_c >= 1 && occ_s >= 1) {
       p->use_r1 = true;
-      p->r1_interp_bytes = ib;
+      p->r1_sort_bytes = cb;
       p->r1_spread_bytes = sb;
     }
     cudaGetLastError();
@@ -414,17 +419,11 @@ void configure_binsort(nfft_plan p) {
   }
 }
 
+// first-generation stable counting sort: count / column scan / scatter (precompute.cuh)
 template <typename R>
-nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
+nfft_status launch_cs3(nfft_plan p, cudaStream_t st) {
   const int M = (int)p->M;
   const int nt = (int)p->n_tiles;
-  CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), st));
-  rec(p, 2, 0);
-  if (p->use_bs) {
-    TRY(launch_binsort<R>(p, st));
-    rec(p, 2, 1);
-    return NFFT_SUCCESS;
-  }
   // stable counting sort into tiles: count, scan (+ offsets, subproblems), scatter (precompute.cuh)
   cs_count_kernel<R><<<p->cs_nblk, CS_W * 32, (size_t)nt * 4, st>>>((const R*)p->d_nodes, p->geom, nt,
                                                                            p->d_cnt, p->d_err);
@@ -439,6 +438,24 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
       (const R*)p->d_nodes, p->geom, nt, p->d_cnt, p->d_offsets, p->d_perm, (R*)p->d_ks);
   ++p->launches;
   CKL();
+  return NFFT_SUCCESS;
+}
+
+template <typename R>
+nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
+  CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), st));
+  rec(p, 2, 0);
+  if (p->use_bs) {
+    TRY(launch_binsort<R>(p, st));
+  } else {
+    TRY(launch_cs3<R>(p, st));
+  }
+  if (p->use_r1) {
+    cellsort_kernel<R, 1><<<(unsigned)p->n_tiles, CST_THREADS, p->r1_sort_bytes, st>>>(
+        p->geom, (const R*)p->d_ks, p->d_perm, p->d_offsets, (R*)p->d_kc, p->d_jc, p->d_ic, p->d_cstart);
+    ++p->launches;
+    CKL();
+  }
   rec(p, 2, 1);
   return NFFT_SUCCESS;
 }
@@ -486,8 +503,9 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
     ks.interp_nd<<<(unsigned)p->n_tiles, RN_THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
   } else if (p->use_r1) {
-    ks.interp1<<<(unsigned)((p->n_tiles + W1_WARPS - 1) / W1_WARPS), W1_THREADS, p->r1_interp_bytes, st>>>(
-        p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
+    const int sharded = p->node_begin > 0 || p->node_end < p->M;
+    ks.interp1<<<(unsigned)((p->M + I1_THREADS - 1) / I1_THREADS), I1_THREADS, 0, st>>>(
+        p->geom, wp, grid, (const T*)p->d_kc, p->d_jc, p->d_ic, p->node_begin, p->node_end, sharded, f);
   } else if (p->tiled) {
     ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
@@ -508,8 +526,10 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   if (p->use_r1) {
     // owner-computes: every grid cell written exactly once, no zero pass
     rec(p, 1, 1);
-    ks.spread1<<<(unsigned)((p->n_tiles + W1_WARPS - 1) / W1_WARPS), W1_THREADS, p->r1_spread_bytes, st>>>(
-        p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, grid);
+    const int sharded = p->node_begin > 0 || p->node_end < p->M;
+    const int segs = (int)((p->Nt[0] + S1_SEG - 1) / S1_SEG);
+    ks.spread1<<<(unsigned)((segs + S1_WARPS - 1) / S1_WARPS), 32 * S1_WARPS, p->r1_spread_bytes, st>>>(
+        p->geom, wp, f, (const T*)p->d_kc, p->d_jc, p->d_ic, p->d_cstart, p->node_begin, p->node_end, sharded, grid);
     ++p->launches;
     CKL();
     return NFFT_SUCCESS;
@@ -725,7 +745,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   for (int d = 0; d < D; ++d) {
     int64_t q = opt.tile[d];
     if (q < 0 || q > Nt[d]) return NFFT_ERROR_BAD_TILE;
-    if (q == 0) q = D == 1 ? 128 : (D == 2 ? 32 : 8);
+    if (q == 0) q = D == 1 ? 512 : (D == 2 ? 32 : 8);
     q = std::min<int64_t>(q, Nt[d]);
     Q[d] = q;
     P[d] = (Nt[d] + q - 1) / q;
@@ -840,6 +860,9 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     ok = alloc((void**)&p->d_cnt, (size_t)n_tiles * p->cs_nblk * 4) && alloc((void**)&p->d_tile_total, n_tiles * 4) &&
          alloc((void**)&p->d_ticket, 16);
   }
+  if (ok && D == 1)
+    ok = alloc(&p->d_kc, (size_t)M * rs) && alloc((void**)&p->d_jc, (size_t)M * 4) &&
+         alloc((void**)&p->d_ic, (size_t)M * 4) && alloc((void**)&p->d_cstart, (size_t)(n_tiles * Q[0] + 1) * 4);
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
   {
     const int bytes = (int)(n_tiles * 4);
