@@ -85,8 +85,8 @@ typedef struct {
   int device;             /* CUDA device ordinal; -1 = current device */
   int method;             /* nfft_method */
   int64_t max_subproblem; /* max nodes per CTA (splits dense tiles); 0 = default */
-  int64_t node_begin;     /* shard [node_begin, node_end) of the TILE-SORTED node order that */
-  int64_t node_end;       /*   forward/adjoint process; node_end = 0 means M (all nodes) */
+  int64_t node_begin;     /* shard [node_begin, node_end) of the plan's SORTED node order (cell order in */
+  int64_t node_end;       /*   cell mode, tile order otherwise) that forward/adjoint process; 0 = M */
   int timing;             /* 1: record CUDA events around every stage (nfft_get_stage_times) */
   int check_nodes;        /* 1 (default): nfft_precompute synchronises once and reports
                              NFFT_ERROR_NONFINITE_NODE; 0: fully asynchronous, no check
@@ -172,9 +172,20 @@ const char* nfft_status_string(nfft_status s);
 /* Ntilde (D entries), tile Q (D), tiles per dim P (D); n_tiles = prod P. Any pointer may be NULL. */
 nfft_status nfft_plan_info(nfft_plan p, int64_t* Ntilde, int64_t* tile, int64_t* tiles_per_dim, int64_t* n_tiles);
 
-/* Copies perm (M int32) and tile offsets (n_tiles+1 int32) to host memory;
- * synchronises the plan stream. Either pointer may be NULL. */
+/* Copies perm (M int32) and tile offsets (n_tiles+1 int32) of the stable sort
+ * into tiles (ties by node index) to host memory; synchronises
+ * the plan stream. Either pointer may be NULL. In cell mode (below) the tile sort
+ * is not part of the hot path and is computed by this call. */
 nfft_status nfft_get_binning(nfft_plan p, int32_t* perm_host, int32_t* tile_offsets_host);
+
+/* Cell mode (methods AUTO and TILED for the dimensions that have cell-sorted
+ * kernels): the precompute sorts the nodes by CELL, i.e. the binning above with
+ * tile = 1 cell per dimension (key = row-major cell index, ties by node index).
+ * order_host (M int32): node index of every sorted position; cstart_host
+ * (prod Ntilde + 1 int32): first sorted position of every cell. Node shards
+ * (options.node_begin/end) index this order. NFFT_ERROR_UNSUPPORTED when the
+ * plan is not in cell mode. Synchronises. */
+nfft_status nfft_get_cell_binning(nfft_plan p, int32_t* order_host, int32_t* cstart_host);
 
 /* Copies the window tables to host: beta^tensor (sum_d N_d doubles, dim 0
  * first) and the polynomial coefficients (D * 2m * (deg+1) doubles,

@@ -26,7 +26,7 @@ NFFT_SYMBOLS = (
     "nfft_default_options", "nfft_plan_create", "nfft_plan_create_ex", "nfft_set_nodes",
     "nfft_precompute", "nfft_forward", "nfft_adjoint", "nfft_plan_destroy", "nfft_status_string",
     "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
-    "nfft_get_launch_count", "nfft_run_stage", "nfft_execute",
+    "nfft_get_launch_count", "nfft_run_stage", "nfft_execute", "nfft_get_cell_binning",
 )
 STAGES = {"precompute": 0, "fwd_deconv": 1, "fwd_fft": 2, "fwd_interp": 3, "adj_spread": 4, "adj_fft": 5,
           "adj_crop": 6}
@@ -81,6 +81,7 @@ def lib():
         "nfft_plan_destroy": [vp],
         "nfft_plan_info": [vp, P(i64), P(i64), P(i64), P(i64)],
         "nfft_get_binning": [vp, P(i32), P(i32)],
+        "nfft_get_cell_binning": [vp, P(i32), P(i32)],
         "nfft_get_window_tables": [vp, P(ctypes.c_double), P(ctypes.c_double), P(c_int)],
         "nfft_get_stage_times": [vp, c_int, P(ctypes.c_float)],
         "nfft_get_launch_count": [vp, P(i64)],
@@ -276,6 +277,24 @@ class NfftPlan:
         _check(lib().nfft_get_binning(self._h, perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                       offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), "nfft_get_binning")
         return perm, offs
+
+    def cell_binning(self):
+        """(order, cstart) of the cell-mode sort (tile = 1 cell), or None when the
+        plan sorts by tiles (include/nfft.h: nfft_get_cell_binning)."""
+        ncells = int(np.prod(self.info()["Ntilde"]))
+        order = np.empty(self.M, np.int32)
+        cstart = np.empty(ncells + 1, np.int32)
+        st = lib().nfft_get_cell_binning(self._h, order.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                         cstart.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+        if st == 9:  # NFFT_ERROR_UNSUPPORTED: tile mode
+            return None
+        _check(st, "nfft_get_cell_binning")
+        return order, cstart
+
+    def sorted_order(self):
+        """Node index of every position of the order node shards refer to."""
+        cb = self.cell_binning()
+        return cb[0] if cb is not None else self.binning()[0]
 
     def window_tables(self):
         deg = ctypes.c_int()

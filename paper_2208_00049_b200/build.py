@@ -59,7 +59,14 @@ def build(force=False, jobs=None, verbose=True):
 
     def compile_one(src):
         obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
-        cmd = [nv] + ARCH + FLAGS + ["-c", src, "-o", obj]
+        dep = obj[:-2] + ".d"
+        if not force and os.path.exists(obj) and os.path.exists(dep):
+            # incremental: skip the translation unit when none of its own inputs changed
+            with open(dep) as fh:
+                files = [f for f in fh.read().replace("\\\n", " ").split()[1:] if os.path.exists(f)]
+            if files and all(os.path.getmtime(f) <= os.path.getmtime(obj) for f in files):
+                return obj
+        cmd = [nv] + ARCH + FLAGS + ["-c", src, "-o", obj, "-MD", "-MF", dep]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")

@@ -20,10 +20,13 @@ struct KernelSet {
   void (*spread_sorted)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
   void (*spread_gather)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
   // D = 1 static-tile kernels (resample1d.cuh)
-  void (*interp1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
-  void (*spread1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, const int*, int, int, int, C*);
+  void (*interp1)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, int, C*);
+  void (*spread1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
   // D = 2, 3 static-tile interpolation (resample_nd.cuh)
   void (*interp_nd)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
+  // D = 2, 3 over cell-sorted nodes (resample_cell.cuh)
+  void (*interp_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
+  void (*spread_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
 };
 
 template <typename T> KernelSet<T> kernels_d1(int m);
@@ -43,18 +46,21 @@ inline KernelSet<T> kernels_for(int D, int m) {
 #include "resample.cuh"
 #include "resample1d.cuh"
 #include "resample_nd.cuh"
+#include "resample_cell.cuh"
 namespace nfftb {
 template <typename T, int D, int M>
 KernelSet<T> make_set() {
   constexpr int DEG = poly_degree(M, sizeof(T) == 8);
   KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
                  interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
-                 spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr};
+                 spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   if constexpr (D == 1) {
     k.interp1 = interp1c_kernel<T, M, DEG>;
     k.spread1 = spread1c_kernel<T, M, DEG>;
   } else {
     k.interp_nd = interp_nd_kernel<T, D, M, DEG>;
+    k.interp_cell = interp_cell_kernel<T, D, M, DEG>;
+    k.spread_cell = spread_cell_kernel<T, D, M, DEG>;
   }
   if constexpr (D <= 2) {
     k.spread_loc = spread_loc_kernel<T, D, M, DEG>;

@@ -22,9 +22,10 @@
 #include "grid.cuh"
 #include "precompute.cuh"
 #include "binsort.cuh"
-#include "cellsort.cuh"
+#include "cellbin.cuh"
 #include "resample1d.cuh"
 #include "resample_nd.cuh"
+#include "resample_cell.cuh"
 
 using namespace nfftb;
 
@@ -81,13 +82,23 @@ struct nfft_plan_s {
   bool use_bs = false;    // one cooperative binsort kernel (binsort.cuh) instead of cs_count/scan/scatter
   int bs_grid = 0, bs_rr = 1;
   size_t bs_bytes = 0;
-  bool use_r1 = false;    // D = 1 cell-sorted interp / owner-computes spread (resample1d.cuh)
   bool use_ind = false;   // D = 2, 3 static-tile interpolation (resample_nd.cuh)
-  size_t r1_sort_bytes = 0, r1_spread_bytes = 0;
-  void* d_kc = nullptr;     // M reals: coordinates in cell order (D = 1)
-  int* d_jc = nullptr;      // M: node index of every cell-sorted position
-  int* d_ic = nullptr;      // M: tile-sorted position of every cell-sorted position (shards)
-  int* d_cstart = nullptr;  // Ntilde + 1: first cell-sorted position of every cell
+  // cell mode (AUTO/TILED): nodes sorted by cell (cellbin.cuh), work tiles defined by the kernels
+  bool cellmode = false;
+  bool tile_binned = false;  // cell mode: perm/offsets (tile sort) computed on demand for nfft_get_binning
+  int64_t ncells = 0;        // prod Ntilde
+  size_t r1_spread_bytes = 0;
+  size_t sc_bytes = 0;       // spread_cell shared memory
+  int sc_cap = 0;            // spread_cell node slots per chunk
+  void* d_kc = nullptr;      // D*M reals: coordinates in cell order (SoA)
+  int* d_jc = nullptr;       // M: node index of every cell-sorted position
+  int* d_cstart = nullptr;   // ncells + 1: first cell-sorted position of every cell
+  int* d_ccount = nullptr;   // ncells: per-cell counters (zero between precomputes)
+  int* d_cslot = nullptr;    // M: slot inside the cell per node; scratch of cl_fix
+  unsigned long long* d_scan_status = nullptr;  // cl_scan look-back state per 4096-cell tile
+  int* d_ctr = nullptr;      // [scan ticket, #small cells, #big cells, -]
+  int* d_small = nullptr;    // cells with 2..CL_SMALL nodes
+  int* d_big = nullptr;      // cells with more nodes
   void* d_grid_in = nullptr;  // B * prod Nt complex: forward input, zero padding persists
   void* d_grid = nullptr;     // B * prod Nt complex: forward FFT output (read by interp)
   void* d_grid_adj = nullptr; // B * prod Nt complex: adjoint grid, all zero between adjoints
@@ -160,7 +171,8 @@ bool is_device_pointer(const void* p) {
 void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
-                  p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_ic, p->d_cstart};
+                  p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
+                  p->d_scan_status, p->d_ctr, p->d_small, p->d_big};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -303,26 +315,52 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
   }
   p->grid_direct = p->sm_count * 8;
-  p->use_r1 = false;
-  if (p->D == 1 && ks.interp1 && (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED)) {
-    const size_t cb = cst_smem_bytes((int)p->Q[0]);
-    const size_t sb = (size_t)S1_WARPS * s1_warp_bytes(p->m, p->csize(), p->rsize());
-    const void* csfn = p->prec == NFFT_COMPLEX128 ? (const void*)cellsort_kernel<double, 1> : (const void*)cellsort_kernel<float, 1>;
-    int occ_c = 0, occ_s = 0;
-    if (cb <= 200 * 1024 &&
-        cudaFuncSetAttribute(csfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb) == cudaSuccess &&
-        cudaFuncSetAttribute((const void*)ks.spread1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, csfn, CST_THREADS, cb) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, 32 * S1_WARPS, sb) == cudaSuccess &&
-        occ_c >= 1 && occ_s >= 1) {
-      p->use_r1 = true;
-      p->r1_sort_bytes = cb;
+  if (p->cellmode) {
+    bool ok = false;
+    if (p->D == 1 && ks.interp1 && ks.spread1) {
+      const size_t sb = (size_t)S1_WARPS * s1_warp_bytes(p->m, p->csize(), p->rsize());
+      int occ_s = 0;
+      ok = cudaFuncSetAttribute((const void*)ks.spread1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) ==
+               cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, 32 * S1_WARPS, sb) ==
+               cudaSuccess &&
+           occ_s >= 1;
       p->r1_spread_bytes = sb;
     }
+    if (p->D >= 2 && ks.interp_cell && ks.spread_cell) {
+      int wrows = 1;
+      for (int d = 0; d < p->D - 1; ++d) wrows *= (int)(p->Q[d] + 2 * p->m - 1);
+      const int wcols = (int)(p->Q[p->D - 1] + 2 * p->m - 1);
+      const int TL = ((2 * p->m + 2 * SC_K - 2) + 1) & ~1;
+      const size_t slot = ((size_t)(p->D - 1) * 2 * p->m + TL + 2) * p->rsize() + 4;
+      const size_t fixed = spread_cell_smem_bytes(p->D, p->m, (int)p->rsize(), 0, wrows, wcols) + 64;
+      const size_t budget = p->D == 2 ? 110 * 1024 : 200 * 1024;
+      int nitems = (int)((p->Q[p->D - 1] + SC_K - 1) / SC_K);
+      int nrows = 1;
+      for (int d = 0; d < p->D - 1; ++d) {
+        nitems *= (int)p->Q[d];
+        nrows *= (int)p->Q[d];
+      }
+      int cap = fixed < budget ? (int)std::min<size_t>(2048, (budget - fixed) / slot) : 0;
+      const size_t sb = spread_cell_smem_bytes(p->D, p->m, (int)p->rsize(), cap, wrows, wcols);
+      int occ_i = 0, occ_s = 0;
+      ok = cap >= 32 && nitems <= 512 && nrows <= 1024 && p->region_bytes <= 200 * 1024 &&
+           cudaFuncSetAttribute((const void*)ks.interp_cell, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->region_bytes) == cudaSuccess &&
+           cudaFuncSetAttribute((const void*)ks.spread_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) ==
+               cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp_cell, RC_THREADS,
+                                                         p->region_bytes) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread_cell, 256, sb) == cudaSuccess &&
+           occ_i >= 1 && occ_s >= 1;
+      p->sc_cap = cap;
+      p->sc_bytes = sb;
+    }
     cudaGetLastError();
+    p->cellmode = ok;
   }
   p->use_ind = false;
-  if (p->D >= 2 && p->tiled && ks.interp_nd &&
+  if (p->D >= 2 && !p->cellmode && p->tiled && ks.interp_nd &&
       (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED)) {
     int occ = 0;
     if (cudaFuncSetAttribute((const void*)ks.interp_nd, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,20 +479,44 @@ nfft_status launch_cs3(nfft_plan p, cudaStream_t st) {
   return NFFT_SUCCESS;
 }
 
+template <typename R, int D>
+nfft_status cell_sort_d(nfft_plan p, cudaStream_t st) {
+  const int M = (int)p->M;
+  const int nc = (int)p->ncells;
+  const int ntiles = (nc + CL_SCAN_TILE - 1) / CL_SCAN_TILE;
+  const unsigned gm = (unsigned)((std::max(M, ntiles) + CL_THREADS - 1) / CL_THREADS);
+  const unsigned gp = (unsigned)((M + CL_THREADS - 1) / CL_THREADS);
+  cl_count_kernel<R, D><<<gm, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_ccount, p->d_cslot, p->d_err,
+                                                   p->d_scan_status, ntiles, p->d_ctr);
+  cl_scan_kernel<<<(unsigned)ntiles, CL_SCAN_THREADS, 0, st>>>(p->d_ccount, nc, p->d_scan_status, p->d_ctr,
+                                                               p->d_cstart);
+  cl_place_kernel<R, D><<<gp, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_cslot, p->d_cstart,
+                                                   (R*)p->d_kc, p->d_jc, p->d_ctr, p->d_small, p->d_big);
+  cl_fix_kernel<R, D><<<(unsigned)(p->sm_count * 4), CL_THREADS, 0, st>>>(
+      p->geom, p->d_cstart, (R*)p->d_kc, p->d_jc, p->d_ctr, p->d_small, p->d_big, p->d_cslot, (R*)p->d_ks);
+  p->launches += 4;
+  CKL();
+  return NFFT_SUCCESS;
+}
+
+template <typename R>
+nfft_status cell_sort(nfft_plan p, cudaStream_t st) {
+  if (p->D == 1) return cell_sort_d<R, 1>(p, st);
+  if (p->D == 2) return cell_sort_d<R, 2>(p, st);
+  return cell_sort_d<R, 3>(p, st);
+}
+
 template <typename R>
 nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
   CK(cudaMemsetAsync(p->d_err, 0, sizeof(int), st));
   rec(p, 2, 0);
-  if (p->use_bs) {
+  if (p->cellmode) {
+    TRY(cell_sort<R>(p, st));
+    p->tile_binned = false;
+  } else if (p->use_bs) {
     TRY(launch_binsort<R>(p, st));
   } else {
     TRY(launch_cs3<R>(p, st));
-  }
-  if (p->use_r1) {
-    cellsort_kernel<R, 1><<<(unsigned)p->n_tiles, CST_THREADS, p->r1_sort_bytes, st>>>(
-        p->geom, (const R*)p->d_ks, p->d_perm, p->d_offsets, (R*)p->d_kc, p->d_jc, p->d_ic, p->d_cstart);
-    ++p->launches;
-    CKL();
   }
   rec(p, 2, 1);
   return NFFT_SUCCESS;
@@ -499,13 +561,16 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   const auto* grid = (const typename cplx<T>::type*)p->d_grid;
-  if (p->use_ind) {
+  if (p->cellmode && p->D >= 2) {
+    ks.interp_cell<<<dim3((unsigned)p->n_tiles, (unsigned)p->B), RC_THREADS, p->region_bytes, st>>>(
+        p->geom, wp, grid, (const T*)p->d_kc, p->d_jc, p->d_cstart, p->node_begin, p->node_end, f);
+  } else if (p->use_ind) {
     ks.interp_nd<<<(unsigned)p->n_tiles, RN_THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
-  } else if (p->use_r1) {
+  } else if (p->cellmode && p->D == 1) {
     const int sharded = p->node_begin > 0 || p->node_end < p->M;
     ks.interp1<<<(unsigned)((p->M + I1_THREADS - 1) / I1_THREADS), I1_THREADS, 0, st>>>(
-        p->geom, wp, grid, (const T*)p->d_kc, p->d_jc, p->d_ic, p->node_begin, p->node_end, sharded, f);
+        p->geom, wp, grid, (const T*)p->d_kc, p->d_jc, p->node_begin, p->node_end, sharded, f);
   } else if (p->tiled) {
     ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
@@ -523,13 +588,22 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   auto* grid = (typename cplx<T>::type*)p->d_grid_adj;  // all zero on entry (plan creation / previous crop)
-  if (p->use_r1) {
+  if (p->cellmode && p->D >= 2) {
+    rec(p, 1, 1);
+    ks.spread_cell<<<dim3((unsigned)p->n_tiles, (unsigned)p->B), 256, p->sc_bytes, st>>>(p->geom, wp, f, (const T*)p->d_kc, p->d_jc,
+                                                                  p->d_cstart, p->node_begin, p->node_end, p->sc_cap,
+                                                                  grid);
+    ++p->launches;
+    CKL();
+    return NFFT_SUCCESS;
+  }
+  if (p->cellmode && p->D == 1) {
     // owner-computes: every grid cell written exactly once, no zero pass
     rec(p, 1, 1);
     const int sharded = p->node_begin > 0 || p->node_end < p->M;
     const int segs = (int)((p->Nt[0] + S1_SEG - 1) / S1_SEG);
     ks.spread1<<<(unsigned)((segs + S1_WARPS - 1) / S1_WARPS), 32 * S1_WARPS, p->r1_spread_bytes, st>>>(
-        p->geom, wp, f, (const T*)p->d_kc, p->d_jc, p->d_ic, p->d_cstart, p->node_begin, p->node_end, sharded, grid);
+        p->geom, wp, f, (const T*)p->d_kc, p->d_jc, p->d_cstart, p->node_begin, p->node_end, sharded, grid);
     ++p->launches;
     CKL();
     return NFFT_SUCCESS;
@@ -568,7 +642,7 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
 template <typename T>
 nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st) {
   const Geom& g = p->geom;
-  if (p->use_r1) {  // the spread rewrites every cell: crop only, no re-zeroing
+  if (p->cellmode) {  // the cell-mode spread rewrites every cell: crop only, no re-zeroing
     const int nl = g.N[g.D - 1];
     const long long rows = (long long)g.B * (g.ngrid_cells / nl);
     dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
@@ -742,11 +816,16 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   const bool c128 = precision == NFFT_COMPLEX128;
   const size_t csz = c128 ? 16 : 8;
   int64_t Q[3] = {1, 1, 1}, P[3] = {1, 1, 1};
+  // cell mode (AUTO/TILED): nodes sorted by cell; Q is the kernels' work tile
+  const bool cell_candidate = opt.method == NFFT_METHOD_AUTO || opt.method == NFFT_METHOD_TILED;
   for (int d = 0; d < D; ++d) {
     int64_t q = opt.tile[d];
     if (q < 0 || q > Nt[d]) return NFFT_ERROR_BAD_TILE;
-    if (q == 0) q = D == 1 ? 512 : (D == 2 ? 32 : 8);
+    if (q == 0) q = D == 1 ? 512 : (D == 2 ? 32 : ((cell_candidate && d == 2) ? 16 : 8));
     q = std::min<int64_t>(q, Nt[d]);
+    // cell-mode spreading reads a window of Q + 2m - 1 cells along the last dimension,
+    // which must not wrap onto itself
+    if (cell_candidate && D >= 2 && d == D - 1) q = std::min<int64_t>(q, Nt[d] - 2 * m + 1);
     Q[d] = q;
     P[d] = (Nt[d] + q - 1) / q;
   }
@@ -860,9 +939,15 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     ok = alloc((void**)&p->d_cnt, (size_t)n_tiles * p->cs_nblk * 4) && alloc((void**)&p->d_tile_total, n_tiles * 4) &&
          alloc((void**)&p->d_ticket, 16);
   }
-  if (ok && D == 1)
-    ok = alloc(&p->d_kc, (size_t)M * rs) && alloc((void**)&p->d_jc, (size_t)M * 4) &&
-         alloc((void**)&p->d_ic, (size_t)M * 4) && alloc((void**)&p->d_cstart, (size_t)(n_tiles * Q[0] + 1) * 4);
+  p->ncells = cells;
+  p->cellmode = cell_candidate;
+  if (ok && p->cellmode)
+    ok = alloc(&p->d_kc, (size_t)M * D * rs) && alloc((void**)&p->d_jc, (size_t)M * 4) &&
+         alloc((void**)&p->d_cstart, (size_t)(cells + 1) * 4) && alloc((void**)&p->d_ccount, (size_t)(cells + 1) * 4) &&
+         alloc((void**)&p->d_cslot, (size_t)M * 4) &&
+         alloc((void**)&p->d_scan_status, (size_t)((cells + CL_SCAN_TILE - 1) / CL_SCAN_TILE + 1) * 8) &&
+         alloc((void**)&p->d_ctr, 16) && alloc((void**)&p->d_small, (size_t)(M / 2 + 1) * 4) &&
+         alloc((void**)&p->d_big, (size_t)(M / (CL_SMALL + 1) + 1) * 4);
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
   {
     const int bytes = (int)(n_tiles * 4);
@@ -884,7 +969,8 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   if (cudaMemsetAsync(p->d_grid_in, 0, (size_t)cells * p->B * csz, p->stream) != cudaSuccess ||
       cudaMemsetAsync(p->d_grid_adj, 0, (size_t)cells * p->B * csz, p->stream) != cudaSuccess ||
 
-      cudaMemsetAsync(p->d_ticket, 0, 16, p->stream) != cudaSuccess)
+      cudaMemsetAsync(p->d_ticket, 0, 16, p->stream) != cudaSuccess ||
+      (p->d_ccount && cudaMemsetAsync(p->d_ccount, 0, (size_t)(cells + 1) * 4, p->stream) != cudaSuccess))
     return fail(NFFT_ERROR_CUDA);
 
   int n[3];
@@ -1079,9 +1165,29 @@ nfft_status nfft_get_binning(nfft_plan p, int32_t* perm_host, int32_t* offsets_h
   if (!p) return NFFT_ERROR_INVALID_VALUE;
   if (!p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
   DeviceGuard guard(p->device);
+  if (p->cellmode && !p->tile_binned) {  // the hot path sorted by cell; the tile sort is computed on demand
+    nfft_status s = p->use_bs ? (p->prec == NFFT_COMPLEX128 ? launch_binsort<double>(p, p->stream)
+                                                            : launch_binsort<float>(p, p->stream))
+                              : (p->prec == NFFT_COMPLEX128 ? launch_cs3<double>(p, p->stream)
+                                                            : launch_cs3<float>(p, p->stream));
+    if (s != NFFT_SUCCESS) return s;
+    p->tile_binned = true;
+  }
   if (perm_host) CK(cudaMemcpyAsync(perm_host, p->d_perm, p->M * 4, cudaMemcpyDeviceToHost, p->stream));
   if (offsets_host)
     CK(cudaMemcpyAsync(offsets_host, p->d_offsets, (p->n_tiles + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return NFFT_SUCCESS;
+}
+
+nfft_status nfft_get_cell_binning(nfft_plan p, int32_t* order_host, int32_t* cstart_host) {
+  if (!p) return NFFT_ERROR_INVALID_VALUE;
+  if (!p->cellmode) return NFFT_ERROR_UNSUPPORTED;
+  if (!p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
+  DeviceGuard guard(p->device);
+  if (order_host) CK(cudaMemcpyAsync(order_host, p->d_jc, p->M * 4, cudaMemcpyDeviceToHost, p->stream));
+  if (cstart_host)
+    CK(cudaMemcpyAsync(cstart_host, p->d_cstart, (p->ncells + 1) * 4, cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   return NFFT_SUCCESS;
 }

@@ -48,15 +48,12 @@ template <typename T, int M, int DEG>
 __global__ void __launch_bounds__(I1_THREADS) interp1c_kernel(Geom g, WinPoly<T> wp,
                                                               const typename cplx<T>::type* __restrict__ grid,
                                                               const T* __restrict__ kc, const int* __restrict__ jc,
-                                                              const int* __restrict__ ic, int nb, int ne, int sharded,
+                                                              int nb, int ne, int sharded,
                                                               typename cplx<T>::type* __restrict__ f) {
   using C = typename cplx<T>::type;
   const int pc = blockIdx.x * I1_THREADS + threadIdx.x;
   if (pc >= g.M) return;
-  if (sharded) {
-    const int i = ic[pc];
-    if (i < nb || i >= ne) return;
-  }
+  if (sharded && (pc < nb || pc >= ne)) return;  // shard = range of the cell-sorted order
   const int j = jc[pc];
   double frac;
   const int Nt = g.Nt[0];
@@ -97,7 +94,6 @@ template <typename T, int M, int DEG>
 __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly<T> wp,
                                                                  const typename cplx<T>::type* __restrict__ f,
                                                                  const T* __restrict__ kc, const int* __restrict__ jc,
-                                                                 const int* __restrict__ ic,
                                                                  const int* __restrict__ cstart, int nb, int ne,
                                                                  int sharded, typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
@@ -186,10 +182,7 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
           ee[u] = e;
           jj[u] = jc[pc];
           kk_[u] = (double)kc[pc];
-          if (sharded) {
-            const int i = ic[pc];
-            if (i < nb || i >= ne) jj[u] = -1;
-          }
+          if (sharded && (pc < nb || pc >= ne)) jj[u] = -1;  // shard = range of the cell-sorted order
         }
       }
       C fvl[SPL];

@@ -252,7 +252,7 @@ def test_shards_sum_to_full_transform():
     for rank in range(3):
         rng = dist.shard_range(w["M"], rank, 3)
         plan = pkg.NfftPlan(nodes, w["N"], m=4, node_range=rng).precompute()
-        perm, _ = plan.binning()
+        perm = plan.sorted_order()
         out = torch.zeros((1, w["M"]), dtype=torch.complex128, device="cuda")
         plan.forward(torch.from_numpy(w["fhat"]).cuda(), out=out)
         mine = perm[rng[0]:rng[1]]
@@ -427,11 +427,30 @@ def test_one_kernel_sort_matches_three_kernel_sort(config):
     """The cooperative binsort (default) and the first-generation three-kernel
     sort (method tiled_v1) give the identical permutation and offsets."""
     w = workloads.make(config, seed=4, batch=1)
-    a = _plan(w)
-    b = _plan(w, method="tiled_v1")
+    tile = {1: (512,), 2: (32, 32), 3: (8, 8, 8)}[len(w["N"])]  # same tiles for both (cell mode widens 3D)
+    a = _plan(w, tile=tile)
+    b = _plan(w, method="tiled_v1", tile=tile)
     pa, oa = a.binning()
     pb, ob = b.binning()
     a.close()
     b.close()
     np.testing.assert_array_equal(pa, pb)
     np.testing.assert_array_equal(oa, ob)
+
+
+@pytest.mark.parametrize("config", ["cfg1_1d_256", "cfg2_1d_2e18", "cfg3_2d_512", "cfg4_3d_64", "cfg5_radial_s2"])
+def test_cell_binning_bit_exact(config):
+    """Cell mode: the hot-path sort is the oracle's binning with tile = 1 cell
+    (key = row-major cell, ties by node index), bit-exact, including the radial
+    centre cell with 402 coincident nodes (dense-cell ordering kernel)."""
+    w = workloads.make(config, seed=0, batch=1)
+    plan = _plan(w)
+    cb = plan.cell_binning()
+    info = plan.info()
+    plan.close()
+    if cb is None:
+        pytest.skip("plan not in cell mode for this D")
+    order, cstart = cb
+    ref_perm, ref_offs, _ = obin.bin_nodes(w["nodes"], info["Ntilde"], tuple(1 for _ in info["Ntilde"]))
+    np.testing.assert_array_equal(order, ref_perm)
+    np.testing.assert_array_equal(cstart, ref_offs)
