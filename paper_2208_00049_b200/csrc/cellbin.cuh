@@ -20,11 +20,11 @@
 //            look-back over 4096-cell tiles, dynamic tile ids), re-zeroes
 //            count[] for the next precompute (no memset).
 //  cl_place  per node: pos = cstart[key] + slot; sorted SoA coordinates
-//            kc[d][pos], node index jc[pos]; cells with >= 2 nodes are listed
-//            (small: <= CL_SMALL nodes, big: more) by their slot-0 node.
-//  cl_fix    listed cells only: node index order inside the cell. Small cells:
-//            one thread, ranks in registers; big cells (the centre of a radial
-//            trajectory): one CTA, ranks by counting smaller indices.
+//            kc[d][pos], node index jc[pos]; cells with > CL_SMALL nodes are
+//            listed by their slot-0 node (rare: the centre of a radial trajectory).
+//  cl_fix    node index order inside every cell with >= 2 nodes: thread per
+//            cell (a coalesced pass over cstart) up to CL_SMALL nodes, ranks in
+//            registers; listed denser cells: one CTA, ranks by counting.
 #pragma once
 
 #include "common.cuh"
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(CL_THREADS) cl_count_kernel(const R* __restric
                                                               int* __restrict__ ctr) {
   const int j = blockIdx.x * CL_THREADS + threadIdx.x;
   if (j < ntiles) status[j] = 0ull;  // scan state of this precompute (read only by cl_scan)
-  if (j < 4) ctr[j] = 0;             // [0] scan ticket, [1] small-cell list, [2] big-cell list
+  if (j < 4) ctr[j] = 0;             // [0] scan ticket, [2] fix-list length
   if (j >= g.M) return;
   R k[MAX_D];
   bool bad;
@@ -88,14 +88,24 @@ __global__ void __launch_bounds__(CL_SCAN_THREADS) cl_scan_kernel(int* __restric
   const int base = tile * CL_SCAN_TILE + threadIdx.x * CL_SCAN_PER;
   int v[CL_SCAN_PER];
   int loc = 0;
+  const bool full = base + CL_SCAN_PER <= n;  // 8 cells, 32-byte aligned: two 16-byte loads and stores
+  if (full) {
+    const int4 a = __ldcg(reinterpret_cast<const int4*>(count + base));
+    const int4 b = __ldcg(reinterpret_cast<const int4*>(count + base) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    if ((a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) != 0) {  // zero for the next precompute
+      reinterpret_cast<int4*>(count + base)[0] = make_int4(0, 0, 0, 0);
+      reinterpret_cast<int4*>(count + base)[1] = make_int4(0, 0, 0, 0);
+    }
+  } else {
 #pragma unroll
-  for (int q = 0; q < CL_SCAN_PER; ++q) {
-    v[q] = base + q < n ? __ldcg(count + base + q) : 0;
-    loc += v[q];
+    for (int q = 0; q < CL_SCAN_PER; ++q) {
+      v[q] = base + q < n ? __ldcg(count + base + q) : 0;
+      if (v[q] != 0) count[base + q] = 0;
+    }
   }
 #pragma unroll
-  for (int q = 0; q < CL_SCAN_PER; ++q)
-    if (base + q < n && v[q] != 0) count[base + q] = 0;  // zero for the next precompute
+  for (int q = 0; q < CL_SCAN_PER; ++q) loc += v[q];
   int agg;
   const int off = block_exclusive_scan(loc, ws, agg);
   if (threadIdx.x < 32) {
@@ -139,10 +149,19 @@ __global__ void __launch_bounds__(CL_SCAN_THREADS) cl_scan_kernel(int* __restric
   }
   __syncthreads();
   int run = excl_s + off;
+  int o[CL_SCAN_PER];
 #pragma unroll
   for (int q = 0; q < CL_SCAN_PER; ++q) {
-    if (base + q < n) cstart[base + q] = run;
+    o[q] = run;
     run += v[q];
+  }
+  if (full) {
+    reinterpret_cast<int4*>(cstart + base)[0] = make_int4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<int4*>(cstart + base)[1] = make_int4(o[4], o[5], o[6], o[7]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < CL_SCAN_PER; ++q)
+      if (base + q < n) cstart[base + q] = o[q];
   }
   if (base <= n && n <= base + CL_SCAN_PER) cstart[n] = excl_s + off + loc;  // thread owning the end
 }
@@ -150,12 +169,12 @@ __global__ void __launch_bounds__(CL_SCAN_THREADS) cl_scan_kernel(int* __restric
 template <typename R, int D>
 __global__ void __launch_bounds__(CL_THREADS) cl_place_kernel(const R* __restrict__ nodes, Geom g,
                                                               const int* __restrict__ slot,
-                                                              const int* __restrict__ cstart, R* __restrict__ kc,
-                                                              int* __restrict__ jc, int* __restrict__ ctr,
-                                                              int* __restrict__ small, int* __restrict__ big) {
+                                                              const int* __restrict__ cstart,
+                                                              R* __restrict__ kc, int* __restrict__ jc,
+                                                              int* __restrict__ ctr, int* __restrict__ fixl) {
   const int j = blockIdx.x * CL_THREADS + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  bool is_small = false, is_big = false;
+  bool listed = false;
   int c = 0;
   if (j < g.M) {
     R k[MAX_D];
@@ -163,45 +182,38 @@ __global__ void __launch_bounds__(CL_THREADS) cl_place_kernel(const R* __restric
     c = cell_key<R, D>(nodes, g, j, k, bad);
     const int s = slot[j];
     const int a = cstart[c], n = cstart[c + 1] - a;
-    const int pos = a + s;
+    const int pos = a + s;  // arrival order inside the cell; cl_fix makes it stable
     jc[pos] = j;
 #pragma unroll
     for (int d = 0; d < D; ++d) kc[(long long)d * g.M + pos] = k[d];
-    is_small = s == 0 && n >= 2 && n <= CL_SMALL;
-    is_big = s == 0 && n > CL_SMALL;
+    listed = s == 0 && n > CL_SMALL;
   }
-  // warp-aggregated appends to the two fix lists
-  const unsigned ms = __ballot_sync(0xffffffffu, is_small), mb = __ballot_sync(0xffffffffu, is_big);
+  const unsigned mb = __ballot_sync(0xffffffffu, listed);
   const unsigned lt = (1u << lane) - 1;
-  if (ms) {
-    int b0 = 0;
-    if (lane == __ffs(ms) - 1) b0 = atomicAdd(ctr + 1, __popc(ms));
-    b0 = __shfl_sync(0xffffffffu, b0, __ffs(ms) - 1);
-    if (is_small) small[b0 + __popc(ms & lt)] = c;
-  }
   if (mb) {
     int b0 = 0;
     if (lane == __ffs(mb) - 1) b0 = atomicAdd(ctr + 2, __popc(mb));
     b0 = __shfl_sync(0xffffffffu, b0, __ffs(mb) - 1);
-    if (is_big) big[b0 + __popc(mb & lt)] = c;
+    if (listed) fixl[b0 + __popc(mb & lt)] = c;
   }
 }
 
-// Stable order inside the listed cells. Small cells: thread per cell (ranks of
-// <= CL_SMALL node indices in registers). Big cells: CTA per cell; n <= 256 *
-// CL_BIGREG in registers + shared memory, larger cells through scratch
-// (sj_out / sk_out: cslot and d_ks, free after cl_place).
+// Stable order (node index) inside every cell with >= 2 nodes. Cells with
+// <= CL_SMALL nodes: thread per cell, found by a coalesced pass over cstart
+// (listing them would serialise ~M/6 appends on one counter), ranks in
+// registers. Listed denser cells: CTA per cell, n <= 256 * CL_BIGREG in
+// registers + shared memory, larger through scratch (sj_out / sk_out: cslot and
+// d_ks, free after cl_place).
 template <typename R, int D>
 __global__ void __launch_bounds__(CL_THREADS) cl_fix_kernel(Geom g, const int* __restrict__ cstart,
-                                                            R* __restrict__ kc, int* __restrict__ jc,
-                                                            const int* __restrict__ ctr,
-                                                            const int* __restrict__ small, const int* __restrict__ big,
+                                                            R* __restrict__ kc, int* __restrict__ jc, int ncells,
+                                                            const int* __restrict__ ctr, const int* __restrict__ big,
                                                             int* __restrict__ sj_out, R* __restrict__ sk_out) {
   __shared__ int sj[CL_THREADS * CL_BIGREG];
-  const int nsmall = ctr[1], nbig = ctr[2];
-  for (int q = blockIdx.x * CL_THREADS + threadIdx.x; q < nsmall; q += gridDim.x * CL_THREADS) {
-    const int c = small[q];
+  const int nbig = ctr[2];
+  for (int c = blockIdx.x * CL_THREADS + threadIdx.x; c < ncells; c += gridDim.x * CL_THREADS) {
     const int a = cstart[c], n = cstart[c + 1] - a;
+    if (n < 2 || n > CL_SMALL) continue;
     int jv[CL_SMALL];
     R kv[CL_SMALL][D];
 #pragma unroll

@@ -97,8 +97,7 @@ struct nfft_plan_s {
   int* d_cslot = nullptr;    // M: slot inside the cell per node; scratch of cl_fix
   unsigned long long* d_scan_status = nullptr;  // cl_scan look-back state per 4096-cell tile
   int* d_ctr = nullptr;      // [scan ticket, #small cells, #big cells, -]
-  int* d_small = nullptr;    // cells with 2..CL_SMALL nodes
-  int* d_big = nullptr;      // cells with more nodes
+  int* d_big = nullptr;      // cells with more than CL_SMALL nodes (cl_fix)
   void* d_grid_in = nullptr;  // B * prod Nt complex: forward input, zero padding persists
   void* d_grid = nullptr;     // B * prod Nt complex: forward FFT output (read by interp)
   void* d_grid_adj = nullptr; // B * prod Nt complex: adjoint grid, all zero between adjoints
@@ -172,7 +171,7 @@ void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
-                  p->d_scan_status, p->d_ctr, p->d_small, p->d_big};
+                  p->d_scan_status, p->d_ctr, p->d_big};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -486,14 +485,20 @@ nfft_status cell_sort_d(nfft_plan p, cudaStream_t st) {
   const int ntiles = (nc + CL_SCAN_TILE - 1) / CL_SCAN_TILE;
   const unsigned gm = (unsigned)((std::max(M, ntiles) + CL_THREADS - 1) / CL_THREADS);
   const unsigned gp = (unsigned)((M + CL_THREADS - 1) / CL_THREADS);
+  static const int stop = getenv("NFFTB_DIAG_PRE_STOP") ? atoi(getenv("NFFTB_DIAG_PRE_STOP")) : 4;  // diagnostic
+  if (stop < 1) return NFFT_SUCCESS;
   cl_count_kernel<R, D><<<gm, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_ccount, p->d_cslot, p->d_err,
                                                    p->d_scan_status, ntiles, p->d_ctr);
+  if (stop < 2) return NFFT_SUCCESS;
   cl_scan_kernel<<<(unsigned)ntiles, CL_SCAN_THREADS, 0, st>>>(p->d_ccount, nc, p->d_scan_status, p->d_ctr,
                                                                p->d_cstart);
+  if (stop < 3) return NFFT_SUCCESS;
   cl_place_kernel<R, D><<<gp, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_cslot, p->d_cstart,
-                                                   (R*)p->d_kc, p->d_jc, p->d_ctr, p->d_small, p->d_big);
-  cl_fix_kernel<R, D><<<(unsigned)(p->sm_count * 4), CL_THREADS, 0, st>>>(
-      p->geom, p->d_cstart, (R*)p->d_kc, p->d_jc, p->d_ctr, p->d_small, p->d_big, p->d_cslot, (R*)p->d_ks);
+                                                   (R*)p->d_kc, p->d_jc, p->d_ctr, p->d_big);
+  if (stop < 4) return NFFT_SUCCESS;
+  const unsigned gf = (unsigned)std::min<int64_t>((nc + CL_THREADS - 1) / CL_THREADS, p->sm_count * 8);
+  cl_fix_kernel<R, D><<<gf, CL_THREADS, 0, st>>>(p->geom, p->d_cstart, (R*)p->d_kc, p->d_jc, nc, p->d_ctr, p->d_big,
+                                                 p->d_cslot, (R*)p->d_ks);
   p->launches += 4;
   CKL();
   return NFFT_SUCCESS;
@@ -946,7 +951,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
          alloc((void**)&p->d_cstart, (size_t)(cells + 1) * 4) && alloc((void**)&p->d_ccount, (size_t)(cells + 1) * 4) &&
          alloc((void**)&p->d_cslot, (size_t)M * 4) &&
          alloc((void**)&p->d_scan_status, (size_t)((cells + CL_SCAN_TILE - 1) / CL_SCAN_TILE + 1) * 8) &&
-         alloc((void**)&p->d_ctr, 16) && alloc((void**)&p->d_small, (size_t)(M / 2 + 1) * 4) &&
+         alloc((void**)&p->d_ctr, 16) &&
          alloc((void**)&p->d_big, (size_t)(M / (CL_SMALL + 1) + 1) * 4);
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
   {

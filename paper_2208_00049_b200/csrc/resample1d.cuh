@@ -30,18 +30,10 @@ namespace nfftb {
 
 constexpr int I1_THREADS = 256;           // interp1c: one node per thread
 constexpr int S1_WARPS = 4;               // spread1c: warps per CTA
-constexpr int S1_K = 4;                   // spread1c: cells per lane
+constexpr int S1_K = 2;                   // spread1c: cells per lane
 constexpr int S1_SEG = 32 * S1_K;         // cells per warp
-constexpr int S1_CAP = 96;                // node slots per warp chunk (typical window: ~0.5 (SEG + 2m) nodes)
+constexpr int S1_CAP = 64;                // node slots per warp chunk (typical window: ~0.5 (SEG + 2m) nodes)
 
-__host__ __device__ inline size_t s1_warp_bytes(int M, size_t csize, size_t rsize) {
-  size_t b = (size_t)S1_CAP * 2 * M * rsize;  // taps per slot
-  b = (b + 15) & ~(size_t)15;
-  b += (size_t)S1_CAP * csize;                // node value of the current batch vector
-  b += (size_t)S1_CAP * 4;                    // extended cell of a slot
-  b += (size_t)(2 * (S1_SEG + 2 * M)) * 4;    // window cell starts, position bases
-  return (b + 15) & ~(size_t)15;
-}
 
 // ---------------------------------------------------------------- forward
 template <typename T, int M, int DEG>
@@ -90,6 +82,36 @@ __global__ void __launch_bounds__(I1_THREADS) interp1c_kernel(Geom g, WinPoly<T>
 }
 
 // ---------------------------------------------------------------- adjoint
+// spread1c: one warp per segment of S1_SEG cells (owner-computes). The warp
+// stages the nodes of its WINDOW (cells [y0 - m, y0 + SEG + m - 2], i.e. every
+// node whose footprint reaches the segment; contiguous cell-sorted ranges from
+// cstart) and spreads them TAP-PARALLEL: the warp is split into groups of G =
+// 8 (m <= 4) or 16 lanes; a group takes one node, lane l evaluates tap l
+// (coefficients of its mirror pair in registers) and adds f_j w_l into cell
+// a - m + 1 + l of the group's private shared-memory accumulator (the G lanes
+// touch G consecutive cells: no conflict, no atomic). The groups' copies are
+// summed when the segment's cells are written, each exactly once, with plain
+// coalesced stores (no zero pass, no halo merge: the paper's locked merge of
+// PAPER.md:578-582 becomes reading the halo NODES).
+template <int M>
+struct S1Cfg {
+  static constexpr int G = 2 * M <= 8 ? 8 : 16;   // lanes per node
+  static constexpr int NG = 32 / G;               // nodes per warp step = accumulator copies
+  static constexpr int NE = S1_SEG + 2 * M - 1;   // window cells (full segment)
+  static constexpr int LEN = NE + 2 * M - 1;      // accumulator cells: window cell e, tap l -> e + l
+};
+
+// shared memory of one spread1c warp (host and device agree)
+__host__ __device__ inline size_t s1_warp_bytes(int M, size_t csize, size_t rsize) {
+  const int G = 2 * M <= 8 ? 8 : 16, NG = 32 / G;
+  const int NE = S1_SEG + 2 * M - 1, LEN = NE + 2 * M - 1;
+  size_t b = (size_t)NG * LEN * csize;                // accumulator copies
+  b += (size_t)S1_CAP * (csize + rsize);              // staged node: value, zeta
+  b += (size_t)S1_CAP * 4;                            // staged node: window cell
+  b += (size_t)(2 * NE + 2) * 4;                      // per window cell: first slot, position base
+  return (b + 15) & ~(size_t)15;
+}
+
 template <typename T, int M, int DEG>
 __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly<T> wp,
                                                                  const typename cplx<T>::type* __restrict__ f,
@@ -97,41 +119,37 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
                                                                  const int* __restrict__ cstart, int nb, int ne,
                                                                  int sharded, typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
-  constexpr int TAPS = 2 * M;
-  constexpr int NEXT = S1_SEG + 2 * M - 1;  // extended cells of a full segment
+  using Cfg = S1Cfg<M>;
+  constexpr int TAPS = 2 * M, G = Cfg::G, NG = Cfg::NG, LEN = Cfg::LEN;
+  constexpr int PER = (Cfg::NE + 1 + 31) / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Nt = g.Nt[0];
   const int y0 = (blockIdx.x * S1_WARPS + warp) * S1_SEG;
   if (y0 >= Nt) return;
   const int nseg = min(S1_SEG, Nt - y0);
-  const int NE = nseg + 2 * M - 1;  // extended cell e <-> binning cell (y0 - m + e) mod Nt
+  const int NE = nseg + 2 * M - 1;  // window cell e <-> binning cell (y0 - m + e) mod Nt
   unsigned char* wb = smem_raw + (size_t)warp * s1_warp_bytes(M, sizeof(C), sizeof(T));
-  T* tap = reinterpret_cast<T*>(wb);  // [S1_CAP][TAPS]
-  C* fv = reinterpret_cast<C*>(wb + (((size_t)S1_CAP * TAPS * sizeof(T) + 15) & ~(size_t)15));
-  int* se = reinterpret_cast<int*>(fv + S1_CAP);  // [S1_CAP] extended cell of the slot
-  int* wstart = se + S1_CAP;                      // [NEXT + 1] first window slot of extended cell e
-  int* wbase = wstart + NEXT + 1;                 // [NEXT] cell-sorted position of slot s = wbase[e] + s
+  C* acc = reinterpret_cast<C*>(wb);                 // [NG][LEN]: cell y0 - 2m + 1 + i
+  C* sv = acc + NG * LEN;                            // [S1_CAP] node value
+  T* sz = reinterpret_cast<T*>(sv + S1_CAP);         // [S1_CAP] zeta = frac - 1/2
+  int* se = reinterpret_cast<int*>(sz + S1_CAP);     // [S1_CAP] window cell
+  int* ws = se + S1_CAP;                             // [NE + 1] first window slot of window cell e
+  int* wbase = ws + Cfg::NE + 1;                     // [NE] position of slot s of cell e = wbase[e] + s
 
-  auto cell_of = [&](int e) {
-    int c = y0 - M + e;
-    if (c < 0) c += Nt;
-    if (c >= Nt) c -= Nt;
-    if ((unsigned)c >= (unsigned)Nt) c = pos_mod(c, Nt);
-    return c;
-  };
-  // window cell starts: all cstart loads of the lane issued together, warp scan;
-  // base[e] = cstart of the cell minus its first window slot; slot -> extended cell map
+  // window slot starts: the lane's cstart loads issued together, warp scan of the counts
+  int total;
   {
-    constexpr int PER = (NEXT + 1 + 31) / 32;
-    const int lo = lane * PER;
     int c_lo[PER], c_hi[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-      const int e = lo + q;
+      const int e = lane * PER + q;
       c_lo[q] = c_hi[q] = 0;
       if (e < NE) {
-        const int c = cell_of(e);
+        int c = y0 - M + e;
+        if (c < 0) c += Nt;
+        if (c >= Nt) c -= Nt;
+        if ((unsigned)c >= (unsigned)Nt) c = pos_mod(c, Nt);
         c_lo[q] = __ldg(cstart + c);
         c_hi[q] = __ldg(cstart + c + 1);
       }
@@ -139,98 +157,114 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
     int sum = 0;
 #pragma unroll
     for (int q = 0; q < PER; ++q) sum += c_hi[q] - c_lo[q];
-    int total;
     int run = warp_exclusive_scan(sum, total);
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-      const int e = lo + q;
-      if (e < NE) {
-        wstart[e] = run;
-        wbase[e] = c_lo[q] - run;
-      }
+      const int e = lane * PER + q;
+      if (e <= NE) ws[e] = run;
+      if (e < NE) wbase[e] = c_lo[q] - run;
       run += c_hi[q] - c_lo[q];
     }
-    if (lane == 0) wstart[NE] = total;
+  }
+  // tap of this lane and the coefficients of its mirror pair (w_l = E + zeta O, w_{2m-1-l} = E - zeta O)
+  const int grp = lane / G, l = lane % G;
+  const bool tap_on = l < TAPS;
+  const int lp = l < M ? l : (TAPS - 1 - l);
+  const T sgn = l < M ? (T)1 : (T)-1;
+  T ce[DEG / 2 + 1], co[(DEG + 1) / 2];
+#pragma unroll
+  for (int z = 0; z <= DEG; ++z) {
+    const T c = tap_on ? wp.mu[0][lp < M ? lp : 0][z] : (T)0;
+    if (z % 2 == 0) ce[z / 2] = c;
+    else co[z / 2] = c;
   }
   __syncwarp();
-  const int total = wstart[NE];
   const int sy0 = pos_mod(y0 - (Nt >> 1), Nt);  // storage of binning cell y0
   for (int b = 0; b < g.B; ++b) {
-    C acc[S1_K];
-#pragma unroll
-    for (int kk = 0; kk < S1_K; ++kk) {
-      acc[kk].x = (T)0;
-      acc[kk].y = (T)0;
+    for (int i = lane; i < NG * LEN; i += 32) {
+      acc[i].x = (T)0;
+      acc[i].y = (T)0;
     }
-    for (int clo = 0; clo < total; clo += S1_CAP) {
+    for (int clo = 0; clo < max(total, 1); clo += S1_CAP) {
       const int chi = min(total, clo + S1_CAP);
-      // slot -> extended cell: each lane marks the slots of its extended cells
-      for (int e = lane; e < NE; e += 32)
-        for (int sl = max(wstart[e], clo); sl < min(wstart[e + 1], chi); ++sl) se[sl - clo] = e;
-      __syncwarp();
-      // node loads of all the lane's slots in flight together, then taps
+      // stage the chunk: window cell, zeta and value of every slot (loads of all the lane's slots in flight)
       constexpr int SPL = (S1_CAP + 31) / 32;
       int jj[SPL], ee[SPL];
-      double kk_[SPL];
+      double kk[SPL];
 #pragma unroll
       for (int u = 0; u < SPL; ++u) {
-        const int sl = lane + 32 * u;
+        const int sl = clo + lane + 32 * u;
+        jj[u] = -1;
         ee[u] = -1;
-        if (clo + sl < chi) {
-          const int e = se[sl];
-          const int pc = wbase[e] + clo + sl;
-          ee[u] = e;
-          jj[u] = jc[pc];
-          kk_[u] = (double)kc[pc];
-          if (sharded && (pc < nb || pc >= ne)) jj[u] = -1;  // shard = range of the cell-sorted order
+        if (sl < chi) {
+          int lo = 0, hi = NE;  // window cell of the slot: last e with ws[e] <= sl
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (ws[mid] <= sl) lo = mid;
+            else hi = mid;
+          }
+          const int pc = wbase[lo] + sl;
+          ee[u] = lo;
+          jj[u] = (sharded && (pc < nb || pc >= ne)) ? -1 : jc[pc];  // shard = range of the cell order
+          kk[u] = (double)kc[pc];
         }
-      }
-      C fvl[SPL];
-#pragma unroll
-      for (int u = 0; u < SPL; ++u) {
-        fvl[u].x = (T)0;
-        fvl[u].y = (T)0;
-        if (ee[u] >= 0 && jj[u] >= 0) fvl[u] = f[(long long)b * g.M + jj[u]];
       }
 #pragma unroll
       for (int u = 0; u < SPL; ++u) {
         const int sl = lane + 32 * u;
-        if (ee[u] < 0) continue;
-        double frac;
-        node_cell(kk_[u], g.Ntd[0], Nt, frac);
-        T w[TAPS];
-        window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
-#pragma unroll
-        for (int l = 0; l < TAPS; ++l) tap[sl * TAPS + l] = w[l];
-        fv[sl] = fvl[u];
+        if (ee[u] >= 0) {
+          C v;
+          v.x = (T)0;
+          v.y = (T)0;
+          if (jj[u] >= 0) v = f[(long long)b * g.M + jj[u]];
+          double frac;
+          node_cell(kk[u], g.Ntd[0], Nt, frac);
+          sv[sl] = v;
+          sz[sl] = (T)(frac - 0.5);
+          se[sl] = ee[u];
+        }
       }
       __syncwarp();
+      // tap-parallel accumulation: group grp takes slots grp, grp + NG, ...
+      C* my = acc + grp * LEN;
+      const int n = chi - clo;
+#pragma unroll 2
+      for (int sl = grp; sl < n; sl += NG) {
+        const T zeta = sz[sl];
+        const C v = sv[sl];
+        const int e = se[sl];
+        const T z2 = zeta * zeta;
+        T ev = ce[DEG / 2];
 #pragma unroll
-      for (int kk = 0; kk < S1_K; ++kk) {
-        const int y = lane + 32 * kk;  // local cell; extended index y + m; contributors e in [y, y + 2m)
-        if (y < nseg) {
-          const int q0 = max(wstart[y], clo), q1 = min(wstart[y + TAPS], chi);
-          for (int q = q0; q < q1; ++q) {
-            const int sl = q - clo;
-            const T wt = tap[sl * TAPS + (y - se[sl] + TAPS - 1)];
-            const C v = fv[sl];
-            acc[kk].x = fma(wt, v.x, acc[kk].x);
-            acc[kk].y = fma(wt, v.y, acc[kk].y);
-          }
+        for (int z = DEG / 2 - 1; z >= 0; --z) ev = fma(ev, z2, ce[z]);
+        T od = co[(DEG - 1) / 2];
+#pragma unroll
+        for (int z = (DEG - 1) / 2 - 1; z >= 0; --z) od = fma(od, z2, co[z]);
+        const T w = fma(sgn * zeta, od, ev);
+        if (tap_on) {
+          C a = my[e + l];
+          a.x = fma(w, v.x, a.x);
+          a.y = fma(w, v.y, a.y);
+          my[e + l] = a;
         }
       }
       __syncwarp();
     }
+    // cell y0 + y <-> accumulator index y + 2m - 1; sum the group copies, one coalesced store per cell
     C* dst = grid + (long long)b * g.grid_cells;
+    for (int y = lane; y < nseg; y += 32) {
+      C a = acc[y + TAPS - 1];
 #pragma unroll
-    for (int kk = 0; kk < S1_K; ++kk) {
-      const int y = lane + 32 * kk;
-      if (y < nseg) {
-        int s = sy0 + y;
-        if (s >= Nt) s -= Nt;
-        dst[s] = acc[kk];
+      for (int q = 1; q < NG; ++q) {
+        const C c = acc[q * LEN + y + TAPS - 1];
+        a.x += c.x;
+        a.y += c.y;
       }
+      int s = sy0 + y;
+      if (s >= Nt) s -= Nt;
+      dst[s] = a;
     }
+    __syncwarp();
   }
 }
 
