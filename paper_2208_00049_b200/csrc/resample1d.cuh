@@ -87,9 +87,10 @@ __global__ void __launch_bounds__(I1_THREADS) interp1c_kernel(Geom g, WinPoly<T>
 // node whose footprint reaches the segment; contiguous cell-sorted ranges from
 // cstart) and spreads them TAP-PARALLEL: the warp is split into groups of G =
 // 8 (m <= 4) or 16 lanes; a group takes one node, lane l evaluates tap l
-// (coefficients of its mirror pair in registers) and adds f_j w_l into cell
-// a - m + 1 + l of the group's private shared-memory accumulator (the G lanes
-// touch G consecutive cells: no conflict, no atomic). The groups' copies are
+// (coefficients of its mirror pair in registers) and the tap is shuffled to
+// the lane that owns its cell: lane q always owns the cells i = q (mod G) of
+// the group's private shared-memory accumulator (no two lanes ever touch the
+// same cell: no conflict, no atomic, no barrier between nodes). The groups' copies are
 // summed when the segment's cells are written, each exactly once, with plain
 // coalesced stores (no zero pass, no halo merge: the paper's locked merge of
 // PAPER.md:578-582 becomes reading the halo NODES).
@@ -225,11 +226,16 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
         }
       }
       __syncwarp();
-      // tap-parallel accumulation: group grp takes slots grp, grp + NG, ...
+      // tap-parallel accumulation: group grp takes slots grp, grp + NG, ...; lane l evaluates tap l,
+      // and the tap is handed (shuffle) to the lane q = (e + t) mod G that always owns the
+      // accumulator cells i = q (mod G): no two lanes ever update the same cell, no barrier.
       C* my = acc + grp * LEN;
       const int n = chi - clo;
+      const int q = l;
 #pragma unroll 2
-      for (int sl = grp; sl < n; sl += NG) {
+      for (int base = 0; base < n; base += NG) {  // uniform trip count (shuffles below)
+        const int sl = min(base + grp, n - 1);
+        const bool valid = base + grp < n;
         const T zeta = sz[sl];
         const C v = sv[sl];
         const int e = se[sl];
@@ -241,11 +247,13 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
 #pragma unroll
         for (int z = (DEG - 1) / 2 - 1; z >= 0; --z) od = fma(od, z2, co[z]);
         const T w = fma(sgn * zeta, od, ev);
-        if (tap_on) {
-          C a = my[e + l];
-          a.x = fma(w, v.x, a.x);
-          a.y = fma(w, v.y, a.y);
-          my[e + l] = a;
+        const int t = (q - e) & (G - 1);
+        const T wt = __shfl_sync(0xffffffffu, w, grp * G + t);
+        if (valid && t < TAPS) {
+          C a = my[e + t];
+          a.x = fma(wt, v.x, a.x);
+          a.y = fma(wt, v.y, a.y);
+          my[e + t] = a;
         }
       }
       __syncwarp();
