@@ -15,7 +15,7 @@ timeout 900 python bench.py "$@" > $out/bench.log 2>&1; rc=$?; echo "bench exit 
 if [ $rc -eq 0 ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file $out/launches.csv python bench.py --steps 3 --warmup 3 --no-sweep --no-e2e --no-cpu "$@" > $out/ncu_launches.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"interp_|spread_" -s 8 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"interp|spread" -s 4 -c 4 \
       -o $out/full python bench.py --steps 3 --warmup 3 --no-sweep --no-e2e --no-cpu "$@" > $out/ncu_full.log 2>&1
   ncu -i $out/full.ncu-rep --page raw --csv > $out/full_raw.csv 2>/dev/null
 fi
