@@ -78,6 +78,16 @@ typedef enum {
                               static-tile interp / owner-computes spread when Q | Ntilde, P >= 3, Q >= 2m) */
 } nfft_method;
 
+/* Window precomputation strategy (Fig. 4 at PAPER.md:748-765). */
+typedef enum {
+  NFFT_PRECOMPUTE_AUTO = 0,       /* POLYNOMIAL (measured faster on B200 at every config) */
+  NFFT_PRECOMPUTE_POLYNOMIAL = 1, /* taps evaluated per call from the piecewise polynomial */
+  NFFT_PRECOMPUTE_TENSOR = 2      /* the 2m D taps of every node stored by nfft_precompute (PAPER.md:599-604,
+                                     "TENSOR": 2m D M reals; trades FP work for memory traffic);
+                                     implemented for the D = 1 cell-mode adjoint (thread per cell
+                                     gather over the stored taps), ignored elsewhere */
+} nfft_precompute_strategy;
+
 typedef struct {
   int64_t batch;          /* B >= 1 transforms sharing the nodes (default 1) */
   int64_t tile[3];        /* block size Q_d in grid cells; 0 = default */
@@ -91,6 +101,8 @@ typedef struct {
   int check_nodes;        /* 1 (default): nfft_precompute synchronises once and reports
                              NFFT_ERROR_NONFINITE_NODE; 0: fully asynchronous, no check
                              (non-finite nodes then give unspecified values, never a fault) */
+  int precompute;         /* nfft_precompute_strategy (default AUTO); TENSOR is used where a kernel
+                             for it exists (D = 1, cell mode) and is ignored elsewhere */
 } nfft_options;
 
 /* Fills *opt with the defaults above. */

@@ -28,6 +28,7 @@ NFFT_SYMBOLS = (
     "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
     "nfft_get_launch_count", "nfft_run_stage", "nfft_execute", "nfft_get_cell_binning",
 )
+PRECOMPUTE = {"auto": 0, "polynomial": 1, "tensor": 2}
 STAGES = {"precompute": 0, "fwd_deconv": 1, "fwd_fft": 2, "fwd_interp": 3, "adj_spread": 4, "adj_fft": 5,
           "adj_crop": 6}
 
@@ -52,7 +53,7 @@ class Options(ctypes.Structure):
         ("batch", ctypes.c_int64), ("tile", ctypes.c_int64 * 3), ("stream", ctypes.c_void_p),
         ("device", ctypes.c_int), ("method", ctypes.c_int), ("max_subproblem", ctypes.c_int64),
         ("node_begin", ctypes.c_int64), ("node_end", ctypes.c_int64), ("timing", ctypes.c_int),
-        ("check_nodes", ctypes.c_int),
+        ("check_nodes", ctypes.c_int), ("precompute", ctypes.c_int),
     ]
 
 
@@ -121,13 +122,15 @@ class NfftPlan:
     nodes: (M, D) float64 (c128) or float32 (c64), torch (any device) or numpy.
     N: grid size per dimension (even). Outputs follow the inputs: torch CUDA in
     -> torch CUDA out; numpy in -> numpy out (host staging inside the library).
-    node_range: (begin, end) shard of the TILE-SORTED node order processed by
-    forward/adjoint (multi-GPU sharding).
+    node_range: (begin, end) shard of the plan's SORTED node order (cell order
+    in cell mode) processed by forward/adjoint (multi-GPU sharding, DESIGN.md
+    §Multi-GPU). precompute: "auto" | "polynomial" | "tensor" (window taps per
+    call vs stored by nfft_precompute).
     """
 
     def __init__(self, nodes, N, m=4, sigma=2.0, precision="c128", batch=1, tile=None, stream=None,
                  device=None, method="auto", max_subproblem=0, node_range=None, timing=False,
-                 check_nodes=True):
+                 check_nodes=True, precompute="auto"):
         L = lib()
         self.N = tuple(int(n) for n in N)
         self.D = len(self.N)
@@ -161,6 +164,7 @@ class NfftPlan:
             opt.node_begin, opt.node_end = int(node_range[0]), int(node_range[1])
         opt.timing = int(bool(timing))
         opt.check_nodes = int(bool(check_nodes))
+        opt.precompute = PRECOMPUTE[precompute]
         self.opts = opt
         Narr = (ctypes.c_int64 * self.D)(*self.N)
         h = ctypes.c_void_p()

@@ -22,6 +22,9 @@ struct KernelSet {
   // D = 1 static-tile kernels (resample1d.cuh)
   void (*interp1)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, int, C*);
   void (*spread1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
+  // D = 1 TENSOR precompute (taps stored by nfft_precompute) and the adjoint over them
+  void (*taps1)(Geom, WinPoly<T>, const T*, T*);
+  void (*spread1t)(Geom, const C*, const T*, const int*, const int*, int, int, int, C*);
   // D = 2, 3 static-tile interpolation (resample_nd.cuh)
   void (*interp_nd)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
   // D = 2, 3 over cell-sorted nodes (resample_cell.cuh)
@@ -53,10 +56,13 @@ KernelSet<T> make_set() {
   constexpr int DEG = poly_degree(M, sizeof(T) == 8);
   KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
                  interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
-                 spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+                 spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                 nullptr, nullptr};
   if constexpr (D == 1) {
     k.interp1 = interp1c_kernel<T, M, DEG>;
     k.spread1 = spread1c_kernel<T, M, DEG>;
+    k.taps1 = taps1_kernel<T, M, DEG>;
+    k.spread1t = spread1t_kernel<T, M>;
   } else {
     k.interp_nd = interp_nd_kernel<T, D, M, DEG>;
     k.interp_cell = interp_cell_kernel<T, D, M, DEG>;

@@ -91,6 +91,8 @@ struct nfft_plan_s {
   size_t sc_bytes = 0;       // spread_cell shared memory
   int sc_cap = 0;            // spread_cell node slots per chunk
   void* d_kc = nullptr;      // D*M reals: coordinates in cell order (SoA)
+  bool tensor = false;       // TENSOR precompute (D = 1 cell mode): taps stored in cell order
+  void* d_wt = nullptr;      // M * 2m reals: taps of every cell-sorted position
   int* d_jc = nullptr;       // M: node index of every cell-sorted position
   int* d_cstart = nullptr;   // ncells + 1: first cell-sorted position of every cell
   int* d_ccount = nullptr;   // ncells: per-cell counters (zero between precomputes)
@@ -171,7 +173,7 @@ void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
-                  p->d_scan_status, p->d_ctr, p->d_big};
+                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -357,6 +359,7 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
     cudaGetLastError();
     p->cellmode = ok;
+    if (!ok) p->tensor = false;
   }
   p->use_ind = false;
   if (p->D >= 2 && !p->cellmode && p->tiled && ks.interp_nd &&
@@ -518,6 +521,14 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
   if (p->cellmode) {
     TRY(cell_sort<R>(p, st));
     p->tile_binned = false;
+    if (p->tensor) {  // TENSOR strategy: the 2m taps of every node, in cell order
+      const KernelSet<R>& ks = kernels_of<R>(p);
+      ks.taps1<<<(unsigned)((p->M + T1_THREADS - 1) / T1_THREADS), T1_THREADS, 0, st>>>(p->geom, poly_of<R>(p),
+                                                                                       (const R*)p->d_kc,
+                                                                                       (R*)p->d_wt);
+      ++p->launches;
+      CKL();
+    }
   } else if (p->use_bs) {
     TRY(launch_binsort<R>(p, st));
   } else {
@@ -598,6 +609,16 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     ks.spread_cell<<<dim3((unsigned)p->n_tiles, (unsigned)p->B), 256, p->sc_bytes, st>>>(p->geom, wp, f, (const T*)p->d_kc, p->d_jc,
                                                                   p->d_cstart, p->node_begin, p->node_end, p->sc_cap,
                                                                   grid);
+    ++p->launches;
+    CKL();
+    return NFFT_SUCCESS;
+  }
+  if (p->cellmode && p->D == 1 && p->tensor) {
+    // TENSOR taps, thread per cell: every grid cell written exactly once, no zero pass
+    rec(p, 1, 1);
+    const int sharded = p->node_begin > 0 || p->node_end < p->M;
+    ks.spread1t<<<(unsigned)((p->Nt[0] + T1_THREADS - 1) / T1_THREADS), T1_THREADS, 0, st>>>(
+        p->geom, f, (const T*)p->d_wt, p->d_jc, p->d_cstart, p->node_begin, p->node_end, sharded, grid);
     ++p->launches;
     CKL();
     return NFFT_SUCCESS;
@@ -800,6 +821,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   if (opt_in) opt = *opt_in;
   if (opt.batch < 1) return NFFT_ERROR_INVALID_VALUE;
   if (opt.method < 0 || opt.method > 7) return NFFT_ERROR_INVALID_VALUE;
+  if (opt.precompute < NFFT_PRECOMPUTE_AUTO || opt.precompute > NFFT_PRECOMPUTE_TENSOR) return NFFT_ERROR_INVALID_VALUE;
   if (!(sigma > 1.0) || !std::isfinite(sigma)) return NFFT_ERROR_BAD_GEOMETRY;
   if (m > MAX_M) return NFFT_ERROR_UNSUPPORTED;
   if (M > (int64_t)0x7fffffff - 1) return NFFT_ERROR_UNSUPPORTED;
@@ -953,6 +975,10 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
          alloc((void**)&p->d_scan_status, (size_t)((cells + CL_SCAN_TILE - 1) / CL_SCAN_TILE + 1) * 8) &&
          alloc((void**)&p->d_ctr, 16) &&
          alloc((void**)&p->d_big, (size_t)(M / (CL_SMALL + 1) + 1) * 4);
+  // TENSOR precompute: the D = 1 cell-mode adjoint, on request (AUTO = POLYNOMIAL: measured
+  // faster on B200)
+  p->tensor = p->cellmode && D == 1 && opt.precompute == NFFT_PRECOMPUTE_TENSOR;
+  if (ok && p->tensor) ok = alloc(&p->d_wt, (size_t)M * 2 * m * rs);
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
   {
     const int bytes = (int)(n_tiles * 4);

@@ -276,4 +276,72 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
   }
 }
 
+// ---------------------------------------------------------------- TENSOR precompute (D = 1)
+// The paper's TENSOR strategy: the 2m window taps of every
+// node are computed once by nfft_precompute and stored in cell order,
+// wt[pos * 2m + t] = psi(frac_pos + m - 1 - t), so the
+// per-call kernels read 8-byte taps instead of evaluating the polynomial.
+constexpr int T1_THREADS = 256;
+
+template <typename T, int M, int DEG>
+__global__ void __launch_bounds__(T1_THREADS) taps1_kernel(Geom g, WinPoly<T> wp, const T* __restrict__ kc,
+                                                           T* __restrict__ wt) {
+  const int pc = blockIdx.x * T1_THREADS + threadIdx.x;
+  if (pc >= g.M) return;
+  double frac;
+  node_cell((double)kc[pc], g.Ntd[0], g.Nt[0], frac);
+  T w[2 * M];
+  window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
+#pragma unroll
+  for (int t = 0; t < 2 * M; ++t) wt[(long long)pc * 2 * M + t] = w[t];
+}
+
+// spread1t: adjoint with TENSOR taps, one thread per grid cell y (owner-computes
+// gather, every cell written exactly once, no shared memory): the nodes of
+// cells x = y - m + i, i = 0..2m-1, are the cell-sorted ranges [cstart[x],
+// cstart[x + 1]) and contribute f_j wt[pos][2m - 1 - i] (static tap index).
+template <typename T, int M>
+__global__ void __launch_bounds__(T1_THREADS) spread1t_kernel(Geom g, const typename cplx<T>::type* __restrict__ f,
+                                                              const T* __restrict__ wt, const int* __restrict__ jc,
+                                                              const int* __restrict__ cstart, int nb, int ne,
+                                                              int sharded, typename cplx<T>::type* __restrict__ grid) {
+  using C = typename cplx<T>::type;
+  constexpr int TAPS = 2 * M;
+  const int y = blockIdx.x * T1_THREADS + threadIdx.x;
+  const int Nt = g.Nt[0];
+  if (y >= Nt) return;
+  int lo[TAPS], hi[TAPS];
+#pragma unroll
+  for (int i = 0; i < TAPS; ++i) {
+    int x = y - M + i;  // binning cell of the i-th contributing cell
+    if (x < 0) x += Nt;
+    if (x >= Nt) x -= Nt;
+    if ((unsigned)x >= (unsigned)Nt) x = pos_mod(x, Nt);
+    lo[i] = __ldg(cstart + x);
+    hi[i] = __ldg(cstart + x + 1);
+    if (sharded) {  // shard = range [nb, ne) of the cell order
+      lo[i] = max(lo[i], nb);
+      hi[i] = min(hi[i], ne);
+    }
+  }
+  int s = y - (Nt >> 1);  // storage of binning cell y
+  if (s < 0) s += Nt;
+  for (int b = 0; b < g.B; ++b) {
+    const C* fb = f + (long long)b * g.M;
+    C acc;
+    acc.x = (T)0;
+    acc.y = (T)0;
+#pragma unroll
+    for (int i = 0; i < TAPS; ++i) {
+      for (int p = lo[i]; p < hi[i]; ++p) {
+        const T w = __ldg(wt + (long long)p * TAPS + (TAPS - 1 - i));
+        const C v = fb[__ldg(jc + p)];
+        acc.x = fma(w, v.x, acc.x);
+        acc.y = fma(w, v.y, acc.y);
+      }
+    }
+    grid[(long long)b * g.grid_cells + s] = acc;
+  }
+}
+
 }  // namespace nfftb

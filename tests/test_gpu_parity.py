@@ -454,3 +454,22 @@ def test_cell_binning_bit_exact(config):
     ref_perm, ref_offs, _ = obin.bin_nodes(w["nodes"], info["Ntilde"], tuple(1 for _ in info["Ntilde"]))
     np.testing.assert_array_equal(order, ref_perm)
     np.testing.assert_array_equal(cstart, ref_offs)
+
+
+@pytest.mark.parametrize("precompute", ["polynomial", "tensor"])
+@pytest.mark.parametrize("case", ["small", "ragged_batch", "dense_cells", "full"])
+def test_1d_precompute_strategies(precompute, case):
+    """D = 1 cell mode with the POLYNOMIAL (taps per call) and TENSOR (taps stored
+    by nfft_precompute) strategies against the oracle: small
+    grid whose spread window wraps the torus several times, batch + ragged
+    tile, many coincident nodes (cells with > 8 nodes), full BASELINE size."""
+    if case == "small":
+        w = workloads.make("cfg1_1d_256", seed=3, N=(20,), M=70, m=4)
+    elif case == "ragged_batch":
+        w = workloads.make("cfg1_1d_256", seed=4, N=(300,), M=700, m=5, batch=3)
+    elif case == "dense_cells":
+        w = workloads.make("cfg1_1d_256", seed=5, N=(64,), M=600, m=3)
+        w["nodes"] = np.round(w["nodes"] * 16) / 16  # 16 distinct on-grid positions
+    else:
+        w = workloads.make("cfg2_1d_2e18", seed=0, m=4)
+    _check(w, precompute=precompute)

@@ -31,7 +31,7 @@ def run(config, m, method="auto", tile=None, steps=20, flush=True, max_subproble
         f = torch.from_numpy(w["f"]).to(dev)
         p = pkg.NfftPlan(nodes, w["N"], m=m, sigma=w["sigma"], precision=w["precision"], batch=w["batch"],
                          tile=tile, stream=st.cuda_stream, method=method, check_nodes=False,
-                         max_subproblem=max_subproblem)
+                         max_subproblem=max_subproblem, precompute=os.environ.get("STAGE_PRECOMPUTE", "auto"))
         fo = torch.empty((w["batch"], w["M"]), dtype=p.tdtype_c, device=dev)
         yo = torch.empty((w["batch"],) + tuple(w["N"]), dtype=p.tdtype_c, device=dev)
         wmb = int(os.environ.get("FLUSH_WRITE_MB", "256"))
