@@ -213,6 +213,13 @@ nfft_status nfft_get_stage_times(nfft_plan p, int which /* 0 forward, 1 adjoint 
  * (cuFFT's kernels are not counted). */
 nfft_status nfft_get_launch_count(nfft_plan p, int64_t* launches);
 
+/* Paths the plan selected at creation (bit set = in use):
+ *   NFFT_FEATURE_CELL_MODE   nodes sorted by cell, cell-mode resampling kernels
+ *   NFFT_FEATURE_TENSOR      TENSOR precompute (stored taps) */
+#define NFFT_FEATURE_CELL_MODE 1
+#define NFFT_FEATURE_TENSOR 4
+nfft_status nfft_get_features(nfft_plan p, int* features);
+
 #ifdef __cplusplus
 }
 #endif

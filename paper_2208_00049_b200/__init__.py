@@ -26,7 +26,7 @@ NFFT_SYMBOLS = (
     "nfft_default_options", "nfft_plan_create", "nfft_plan_create_ex", "nfft_set_nodes",
     "nfft_precompute", "nfft_forward", "nfft_adjoint", "nfft_plan_destroy", "nfft_status_string",
     "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
-    "nfft_get_launch_count", "nfft_run_stage", "nfft_execute", "nfft_get_cell_binning",
+    "nfft_get_launch_count", "nfft_run_stage", "nfft_execute", "nfft_get_cell_binning", "nfft_get_features",
 )
 PRECOMPUTE = {"auto": 0, "polynomial": 1, "tensor": 2}
 STAGES = {"precompute": 0, "fwd_deconv": 1, "fwd_fft": 2, "fwd_interp": 3, "adj_spread": 4, "adj_fft": 5,
@@ -86,6 +86,7 @@ def lib():
         "nfft_get_window_tables": [vp, P(ctypes.c_double), P(ctypes.c_double), P(c_int)],
         "nfft_get_stage_times": [vp, c_int, P(ctypes.c_float)],
         "nfft_get_launch_count": [vp, P(i64)],
+        "nfft_get_features": [vp, P(c_int)],
         "nfft_run_stage": [vp, c_int, vp, vp],
         "nfft_execute": [vp, c_int, vp, vp, vp, vp],
     }
@@ -314,6 +315,12 @@ class NfftPlan:
         ms = (ctypes.c_float * 5)()
         _check(lib().nfft_get_stage_times(self._h, 0 if which == "forward" else 1, ms), "nfft_get_stage_times")
         return dict(deconv=ms[0], fft=ms[1], resample=ms[2], zero=ms[3], precompute=ms[4])
+
+    def features(self):
+        """Paths in use: {"cell_mode", "tensor"} (include/nfft.h: nfft_get_features)."""
+        v = ctypes.c_int()
+        _check(lib().nfft_get_features(self._h, ctypes.byref(v)), "nfft_get_features")
+        return {k for k, bit in (("cell_mode", 1), ("tensor", 4)) if v.value & bit}
 
     def launches(self):
         n = ctypes.c_int64()

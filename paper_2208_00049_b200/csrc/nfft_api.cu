@@ -1278,6 +1278,12 @@ nfft_status nfft_get_stage_times(nfft_plan p, int which, float* ms) {
   return NFFT_SUCCESS;
 }
 
+nfft_status nfft_get_features(nfft_plan p, int* features) {
+  if (!p || !features) return NFFT_ERROR_INVALID_VALUE;
+  *features = (p->cellmode ? NFFT_FEATURE_CELL_MODE : 0) | (p->tensor ? NFFT_FEATURE_TENSOR : 0);
+  return NFFT_SUCCESS;
+}
+
 nfft_status nfft_get_launch_count(nfft_plan p, int64_t* launches) {
   if (!p || !launches) return NFFT_ERROR_INVALID_VALUE;
   *launches = p->launches;

@@ -472,4 +472,8 @@ def test_1d_precompute_strategies(precompute, case):
         w["nodes"] = np.round(w["nodes"] * 16) / 16  # 16 distinct on-grid positions
     else:
         w = workloads.make("cfg2_1d_2e18", seed=0, m=4)
+    plan = _plan(w, precompute=precompute)
+    feats = plan.features()
+    plan.close()
+    assert "cell_mode" in feats and (("tensor" in feats) == (precompute == "tensor")), feats
     _check(w, precompute=precompute)
