@@ -38,7 +38,7 @@ constexpr int SC_K = 4;          // spread_cell: consecutive last-dimension cell
 
 // ---------------------------------------------------------------- forward
 template <typename T, int D, int M, int DEG>
-__global__ void __launch_bounds__(RC_THREADS) interp_cell_kernel(Geom g, WinPoly<T> wp,
+__global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel(Geom g, WinPoly<T> wp,
                                                                  const typename cplx<T>::type* __restrict__ grid,
                                                                  const T* __restrict__ kc, const int* __restrict__ jc,
                                                                  const int* __restrict__ cstart, int nb, int ne,
