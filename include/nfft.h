@@ -215,9 +215,11 @@ nfft_status nfft_get_launch_count(nfft_plan p, int64_t* launches);
 
 /* Paths the plan selected at creation (bit set = in use):
  *   NFFT_FEATURE_CELL_MODE   nodes sorted by cell, cell-mode resampling kernels
- *   NFFT_FEATURE_TENSOR      TENSOR precompute (stored taps) */
+ *   NFFT_FEATURE_TENSOR      TENSOR precompute (stored taps)
+ *   NFFT_FEATURE_BATCH       2D batch adjoint: row segments, lanes = batch vectors (B >= 8) */
 #define NFFT_FEATURE_CELL_MODE 1
 #define NFFT_FEATURE_TENSOR 4
+#define NFFT_FEATURE_BATCH 8
 nfft_status nfft_get_features(nfft_plan p, int* features);
 
 #ifdef __cplusplus

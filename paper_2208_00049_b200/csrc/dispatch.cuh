@@ -30,6 +30,9 @@ struct KernelSet {
   // D = 2, 3 over cell-sorted nodes (resample_cell.cuh)
   void (*interp_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
   void (*spread_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
+  // D = 2 batches: row-segment spread, lanes = batch vectors (resample_rowbatch.cuh)
+  void (*spread_rowbatch)(Geom, const C*, int, const T*, const T*, const int*, const int*, C*);
+  void (*taps_nd)(Geom, WinPoly<T>, const T*, T*);
 };
 
 template <typename T> KernelSet<T> kernels_d1(int m);
@@ -50,6 +53,7 @@ inline KernelSet<T> kernels_for(int D, int m) {
 #include "resample1d.cuh"
 #include "resample_nd.cuh"
 #include "resample_cell.cuh"
+#include "resample_rowbatch.cuh"
 namespace nfftb {
 template <typename T, int D, int M>
 KernelSet<T> make_set() {
@@ -57,7 +61,7 @@ KernelSet<T> make_set() {
   KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
                  interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
                  spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                 nullptr, nullptr};
+                 nullptr, nullptr, nullptr, nullptr};
   if constexpr (D == 1) {
     k.interp1 = interp1c_kernel<T, M, DEG>;
     k.spread1 = spread1c_kernel<T, M, DEG>;
@@ -67,6 +71,8 @@ KernelSet<T> make_set() {
     k.interp_nd = interp_nd_kernel<T, D, M, DEG>;
     k.interp_cell = interp_cell_kernel<T, D, M, DEG>;
     k.spread_cell = spread_cell_kernel<T, D, M, DEG>;
+    if constexpr (D == 2) k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
+    k.taps_nd = taps_nd_kernel<T, D, M, DEG>;
   }
   if constexpr (D <= 2) {
     k.spread_loc = spread_loc_kernel<T, D, M, DEG>;

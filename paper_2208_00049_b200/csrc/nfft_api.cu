@@ -26,6 +26,7 @@
 #include "resample1d.cuh"
 #include "resample_nd.cuh"
 #include "resample_cell.cuh"
+#include "resample_rowbatch.cuh"
 
 using namespace nfftb;
 
@@ -92,6 +93,11 @@ struct nfft_plan_s {
   int sc_cap = 0;            // spread_cell node slots per chunk
   void* d_kc = nullptr;      // D*M reals: coordinates in cell order (SoA)
   bool tensor = false;       // TENSOR precompute (D = 1 cell mode): taps stored in cell order
+  bool batchmode = false;    // D = 2 cell mode, B >= 8: row-segment spread with lanes = batch vectors
+  int bp = 0;                // batch padded to a multiple of 32
+  void* d_fT = nullptr;      // M * bp complex: node values, transposed (node-major)
+  size_t rb_bytes = 0;
+
   void* d_wt = nullptr;      // M * 2m reals: taps of every cell-sorted position
   int* d_jc = nullptr;       // M: node index of every cell-sorted position
   int* d_cstart = nullptr;   // ncells + 1: first cell-sorted position of every cell
@@ -173,7 +179,7 @@ void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
-                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt};
+                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -361,6 +367,20 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     p->cellmode = ok;
     if (!ok) p->tensor = false;
   }
+  if (p->batchmode) {
+    bool ok = p->cellmode && ks.spread_rowbatch;
+    if (ok) {
+      p->rb_bytes = rb_smem_bytes(p->m, (int)p->rsize());
+      int o = 0;
+      ok = cudaFuncSetAttribute((const void*)ks.spread_rowbatch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->rb_bytes) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void*)ks.spread_rowbatch, RB_THREADS, p->rb_bytes) ==
+               cudaSuccess &&
+           o >= 1;
+      cudaGetLastError();
+    }
+    p->batchmode = ok;
+  }
   p->use_ind = false;
   if (p->D >= 2 && !p->cellmode && p->tiled && ks.interp_nd &&
       (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED)) {
@@ -521,6 +541,13 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
   if (p->cellmode) {
     TRY(cell_sort<R>(p, st));
     p->tile_binned = false;
+    if (p->batchmode) {  // taps of every node for the batch adjoint (TENSOR layout)
+      const KernelSet<R>& ks = kernels_of<R>(p);
+      ks.taps_nd<<<(unsigned)((p->M + 255) / 256), 256, 0, st>>>(p->geom, poly_of<R>(p), (const R*)p->d_kc,
+                                                                 (R*)p->d_wt);
+      ++p->launches;
+      CKL();
+    }
     if (p->tensor) {  // TENSOR strategy: the 2m taps of every node, in cell order
       const KernelSet<R>& ks = kernels_of<R>(p);
       ks.taps1<<<(unsigned)((p->M + T1_THREADS - 1) / T1_THREADS), T1_THREADS, 0, st>>>(p->geom, poly_of<R>(p),
@@ -604,6 +631,19 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   auto* grid = (typename cplx<T>::type*)p->d_grid_adj;  // all zero on entry (plan creation / previous crop)
+  if (p->batchmode) {
+    using C = typename cplx<T>::type;
+    rec(p, 1, 1);
+    const unsigned nch = (unsigned)(p->bp / RB_LANES);
+    transpose_bm_kernel<T><<<dim3((unsigned)((p->M + 31) / 32), nch), 256, 0, st>>>(f, (int)p->B, (int)p->M, p->bp,
+                                                                                   (C*)p->d_fT);
+    const unsigned segs = (unsigned)(p->Nt[0] * ((p->Nt[1] + RB_SEG - 1) / RB_SEG));
+    ks.spread_rowbatch<<<dim3(segs, nch), RB_THREADS, p->rb_bytes, st>>>(
+        p->geom, (const C*)p->d_fT, p->bp, (const T*)p->d_kc, (const T*)p->d_wt, p->d_jc, p->d_cstart, grid);
+    p->launches += 2;
+    CKL();
+    return NFFT_SUCCESS;
+  }
   if (p->cellmode && p->D >= 2) {
     rec(p, 1, 1);
     ks.spread_cell<<<dim3((unsigned)p->n_tiles, (unsigned)p->B), 256, p->sc_bytes, st>>>(p->geom, wp, f, (const T*)p->d_kc, p->d_jc,
@@ -979,6 +1019,13 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   // faster on B200)
   p->tensor = p->cellmode && D == 1 && opt.precompute == NFFT_PRECOMPUTE_TENSOR;
   if (ok && p->tensor) ok = alloc(&p->d_wt, (size_t)M * 2 * m * rs);
+  // 2D batches of >= 8 transforms: row-segment adjoint with lanes = batch vectors (not for node
+  // shards; the 16 + 2m - 1 window columns must not wrap onto themselves)
+  p->batchmode = p->cellmode && D == 2 && p->B >= 8 && opt.node_begin == 0 && (opt.node_end == 0 || opt.node_end == M) &&
+                 Nt[1] >= RB_SEG + 2 * m - 1 && !getenv("NFFTB_NO_BATCH_KERNELS");
+  p->bp = (int)((p->B + 31) / 32 * 32);
+  if (ok && p->batchmode)
+    ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && alloc(&p->d_wt, (size_t)M * D * 2 * m * rs);
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
   {
     const int bytes = (int)(n_tiles * 4);
@@ -1280,7 +1327,8 @@ nfft_status nfft_get_stage_times(nfft_plan p, int which, float* ms) {
 
 nfft_status nfft_get_features(nfft_plan p, int* features) {
   if (!p || !features) return NFFT_ERROR_INVALID_VALUE;
-  *features = (p->cellmode ? NFFT_FEATURE_CELL_MODE : 0) | (p->tensor ? NFFT_FEATURE_TENSOR : 0);
+  *features = (p->cellmode ? NFFT_FEATURE_CELL_MODE : 0) | (p->tensor ? NFFT_FEATURE_TENSOR : 0) |
+              (p->batchmode ? NFFT_FEATURE_BATCH : 0);
   return NFFT_SUCCESS;
 }
 

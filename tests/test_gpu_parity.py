@@ -477,3 +477,23 @@ def test_1d_precompute_strategies(precompute, case):
     plan.close()
     assert "cell_mode" in feats and (("tensor" in feats) == (precompute == "tensor")), feats
     _check(w, precompute=precompute)
+
+
+@pytest.mark.parametrize("case", ["2d_c64_b32", "2d_c128_b9", "radial_b33_s125", "2d_c64_b8_m8"])
+def test_batch_adjoint(case):
+    """2D batches of >= 8 transforms: row-segment adjoint with lanes = batch
+    vectors (resample_rowbatch.cuh); every vector against the oracle, ragged
+    chunks (B = 9, 33), wrapped windows, c64 and c128."""
+    if case == "2d_c64_b32":
+        w = workloads.make("cfg5_radial_s2", seed=13, N=(40, 36), M=1200, m=4, batch=32)
+    elif case == "2d_c128_b9":
+        w = workloads.make("cfg3_2d_512", seed=14, N=(48, 40), M=1500, m=3, batch=9)
+    elif case == "2d_c64_b8_m8":
+        w = workloads.make("cfg5_radial_s2", seed=17, N=(48, 64), M=900, m=8, batch=8)
+    else:
+        w = workloads.make("cfg5_radial_s125", seed=16, N=(64, 64), M=2000, m=4, batch=33)
+    plan = _plan(w)
+    feats = plan.features()
+    plan.close()
+    assert "batch" in feats, feats
+    _check(w)
