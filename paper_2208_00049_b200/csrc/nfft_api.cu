@@ -841,6 +841,16 @@ nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, 
   return NFFT_SUCCESS;
 }
 
+// nfft_execute: the adjoint chain (spread -> FFT -> crop) is the longer one, so its internal
+// stream gets the highest priority (its CTAs are scheduled first when both chains compete);
+// NFFTB_ADJ_PRIORITY=0 keeps the default priority (diagnostic).
+static int adj_priority() {
+  int lo = 0, hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return 0;
+  const char* e = getenv("NFFTB_ADJ_PRIORITY");
+  return (e && atoi(e) == 0) ? lo : hi;
+}
+
 nfft_status copy_nodes(nfft_plan p, const void* nodes) {
   const size_t bytes = (size_t)p->M * p->D * p->rsize();
   CK(cudaMemcpyAsync(p->d_nodes, nodes, bytes, is_device_pointer(nodes) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
@@ -1063,7 +1073,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     return fail(NFFT_ERROR_CUFFT);
   p->fft_adj_ok = true;
   if (cudaStreamCreateWithFlags(&p->side_pre, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&p->side_adj, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&p->side_adj, cudaStreamNonBlocking, adj_priority()) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_pre, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_adj, cudaEventDisableTiming) != cudaSuccess)
