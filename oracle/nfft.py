@@ -22,13 +22,18 @@ import numpy as np
 from . import window
 
 
-def geometry(N, sigma, m):
+def geometry(N, sigma, m, window_points="2m"):
     """Plan geometry (readings R3/R4).
 
     Ntilde_d = 2 ceil(sigma N_d / 2); beta_d = pi m (2 - N_d / Ntilde_d).
     Raises ValueError on the invalid geometries DESIGN.md lists (odd N_d,
-    sigma <= 1, 2m >= Ntilde_d).
+    sigma <= 1, 2m >= Ntilde_d; 2m+2 >= Ntilde_d for the 2m+2 variant).
+    window_points: "2m" (the paper's truncated psi_hat) or
+    "2m+2" (NFFT3's variant: 2m+2 samples of the continued
+    window, same shape beta and correction).
     """
+    if window_points not in ("2m", "2m+2"):
+        raise ValueError("window_points must be '2m' or '2m+2'")
     N = tuple(int(n) for n in N)
     if sigma <= 1.0:
         raise ValueError("sigma must be > 1")
@@ -39,11 +44,12 @@ def geometry(N, sigma, m):
         if n < 2 or n % 2:
             raise ValueError("N_d must be even and >= 2")
         Ntilde.append(2 * math.ceil(sigma * n / 2.0))
+    npts = 2 * m if window_points == "2m" else 2 * m + 2
     for nt in Ntilde:
-        if 2 * m >= nt:
-            raise ValueError("2m must be < Ntilde_d")
+        if npts >= nt:
+            raise ValueError("the footprint (2m or 2m+2 cells) must be < Ntilde_d")
     beta = [window.kb_beta(m, nt / n) for n, nt in zip(N, Ntilde)]
-    return {"D": len(N), "N": N, "Ntilde": tuple(Ntilde), "m": int(m), "beta": beta}
+    return {"D": len(N), "N": N, "Ntilde": tuple(Ntilde), "m": int(m), "beta": beta, "points": npts}
 
 
 def _logical_axes(N):
@@ -88,27 +94,33 @@ def fft_adjoint(ghat):
     return np.fft.ifftn(ghat) * float(np.prod(ghat.shape))
 
 
-def local_taps(k_d, Ntilde_d, m, beta_d):
+def local_taps(k_d, Ntilde_d, m, beta_d, points=None):
     """Per-dimension footprint and window values of every node (PAPER.md:489-492,
     reading R7: the unwrapped index l enters the window argument).
 
     Returns (l0, W): l0 = floor(Ntilde_d k_d) - m + 1 (first footprint index,
     unwrapped) and W[ell] = psi_hat_Base((Ntilde_d k_d - (l0 + ell)) / m),
-    ell = 0..2m-1.
+    ell = 0..2m-1. With points = 2m+2 (NFFT3 variant): l0 =
+    floor(Ntilde_d k_d) - m, ell = 0..2m+1, and the continued window
+    phi_hat (window.phi_hat_continued) in place of psi_hat.
     """
+    points = 2 * m if points is None else points
     t = Ntilde_d * np.asarray(k_d, np.float64)
     a = np.floor(t)
-    l0 = a.astype(np.int64) - m + 1
-    W = np.empty((2 * m, t.shape[0]), dtype=np.float64)
-    for ell in range(2 * m):
-        W[ell] = window.psi_hat_base((t - (a - m + 1 + ell)) / m, beta_d)
+    first = a - m + 1 if points == 2 * m else a - m
+    l0 = first.astype(np.int64)
+    W = np.empty((points, t.shape[0]), dtype=np.float64)
+    for ell in range(points):
+        u = (t - (first + ell)) / m
+        W[ell] = window.psi_hat_base(u, beta_d) if points == 2 * m else window.phi_hat_continued(u, beta_d)
     return l0, W
 
 
 def _footprints(nodes, geom):
     D, m = geom["D"], geom["m"]
-    taps = [local_taps(nodes[:, d], geom["Ntilde"][d], m, geom["beta"][d]) for d in range(D)]
-    for ell in itertools.product(range(2 * m), repeat=D):
+    P = geom.get("points", 2 * m)
+    taps = [local_taps(nodes[:, d], geom["Ntilde"][d], m, geom["beta"][d], P) for d in range(D)]
+    for ell in itertools.product(range(P), repeat=D):
         w = np.ones(nodes.shape[0], dtype=np.float64)
         flat = np.zeros(nodes.shape[0], dtype=np.int64)
         for d in range(D):
@@ -145,13 +157,13 @@ def resample_adjoint(f, nodes, geom):
     return (re + 1j * im).reshape(geom["Ntilde"])
 
 
-def forward(nodes, fhat, N, m, sigma, rows=None):
+def forward(nodes, fhat, N, m, sigma, rows=None, window_points="2m"):
     """Direct NFFT, Alg. 1: N-grid fhat -> M node values.
 
     `fhat` has shape N or (B, *N); the result has shape (M,) or (B, M).
     `rows` (optional index array) evaluates only those nodes (the grid steps
-    are still done in full)."""
-    geom = geometry(N, sigma, m)
+    are still done in full). window_points: see geometry()."""
+    geom = geometry(N, sigma, m, window_points)
     nodes = np.asarray(nodes, np.float64).reshape(-1, geom["D"])
     if rows is not None:
         nodes = nodes[np.asarray(rows)]
@@ -167,11 +179,12 @@ def forward(nodes, fhat, N, m, sigma, rows=None):
     return out if batched else out[0]
 
 
-def adjoint(nodes, f, N, m, sigma):
+def adjoint(nodes, f, N, m, sigma, window_points="2m"):
     """Adjoint NFFT, Alg. 2: M node values -> N-grid y.
 
-    `f` has shape (M,) or (B, M); the result has shape N or (B, *N)."""
-    geom = geometry(N, sigma, m)
+    `f` has shape (M,) or (B, M); the result has shape N or (B, *N).
+    window_points: see geometry()."""
+    geom = geometry(N, sigma, m, window_points)
     nodes = np.asarray(nodes, np.float64).reshape(-1, geom["D"])
     f = np.asarray(f, np.complex128)
     batched = f.ndim == 2

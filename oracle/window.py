@@ -65,6 +65,20 @@ def phi_hat_base(u, beta):
     return out
 
 
+def phi_hat_continued(u, beta):
+    """phi_hat_Base continued analytically beyond |u| = 1 (the NFFT3 window the
+    paper contrasts with its own: sampled at 2m+2 points "using
+    phi_hat instead of psi_hat"): sinh(beta s)/(pi s), s = sqrt(1-u^2), for
+    |u| < 1, beta/pi at |u| = 1, and with s = i sqrt(u^2-1) for |u| > 1,
+    sin(beta sqrt(u^2-1)) / (pi sqrt(u^2-1))."""
+    u = np.asarray(u, dtype=np.float64)
+    out = phi_hat_base(u, beta)
+    outside = np.abs(u) > 1.0
+    s = np.sqrt(u[outside] ** 2 - 1.0)
+    out[outside] = np.sin(beta * s) / (math.pi * s)
+    return out
+
+
 def psi_hat_base(u, beta):
     """Truncated window psi_hat_Base: phi_hat_Base on the half-open [-1, 1)
     and 0 elsewhere ("truncated to [-1,1)")."""

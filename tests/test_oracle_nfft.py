@@ -215,3 +215,50 @@ def test_full_size_1d_row_sampled_against_ndft():
     ref = ndft.ndft_rows(w["nodes"], w["fhat"][0], w["N"], rows)
     got = nfft.forward(w["nodes"], w["fhat"][0], w["N"], 8, 2.0, rows=rows)
     assert rel_l2(got, ref) < 1e-13
+
+
+# ---------------------------------------------------------------- 2m+2 window variant
+
+def test_continued_window_is_the_analytic_continuation():
+    """phi_hat_continued: the sinh form inside |u| < 1, continuous at |u| = 1
+    (limit beta/pi from both sides), and outside equal to sinh(beta s)/(pi s)
+    evaluated with the complex root s = i sqrt(u^2 - 1)."""
+    from oracle import window
+    beta = window.kb_beta(4, 2.0)
+    u_in = np.linspace(-0.999, 0.999, 101)
+    np.testing.assert_allclose(window.phi_hat_continued(u_in, beta), window.phi_hat_base(u_in, beta), rtol=1e-15)
+    for side in (1 - 1e-9, 1 + 1e-9, -(1 - 1e-9), -(1 + 1e-9)):
+        v = window.phi_hat_continued(np.array([side]), beta)[0]
+        assert abs(v - beta / np.pi) < 1e-6 * beta / np.pi
+    u_out = np.concatenate([np.linspace(1.001, 1.3, 50), -np.linspace(1.001, 1.3, 50)])
+    s = np.sqrt((1 - u_out ** 2).astype(np.complex128))
+    ref = (np.sinh(beta * s) / (np.pi * s)).real
+    np.testing.assert_allclose(window.phi_hat_continued(u_out, beta), ref, rtol=1e-12, atol=1e-12 * beta)
+
+
+@pytest.mark.parametrize("m", [3, 4, 5, 6])
+def test_window_2m_plus_2_accuracy_matches_the_paper(m):
+    """sampling the continued window at 2m+2 points is
+    (slightly) more accurate than the paper's 2m points at the same m, but
+    increasing m by one with 2m points is much more accurate than both
+    (config 1, sigma = 2, against the exact NDFT; measured ratios 1.4-2x and
+    ~90x at these m)."""
+    w = workloads.make("cfg1_1d_256", seed=0)
+    x, fh, f, N = w["nodes"], w["fhat"][0], w["f"][0], w["N"]
+    ex, ey = ndft.ndft(x, fh, N), ndft.adjoint_ndft(x, f, N)
+    e = {}
+    for pts, mm in (("2m", m), ("2m+2", m), ("2m", m + 1)):
+        e[pts, mm] = (rel_l2(nfft.forward(x, fh, N, mm, 2.0, window_points=pts), ex),
+                      rel_l2(nfft.adjoint(x, f, N, mm, 2.0, window_points=pts), ey))
+    for k in (0, 1):
+        assert e["2m+2", m][k] < e["2m", m][k]
+        assert e["2m", m + 1][k] < e["2m+2", m][k] / 10
+
+
+def test_window_2m_plus_2_adjoint_identity():
+    """<A fhat, f> = <fhat, A^H f> for the 2m+2 variant (both sides use the same taps)."""
+    nodes, fhat, f = _rand(31, 300, (24, 20))
+    Af = nfft.forward(nodes, fhat, (24, 20), 3, 2.0, window_points="2m+2")
+    AHf = nfft.adjoint(nodes, f, (24, 20), 3, 2.0, window_points="2m+2")
+    lhs, rhs = np.vdot(f, Af), np.vdot(AHf, fhat)
+    assert abs(lhs - rhs) / (np.linalg.norm(Af) * np.linalg.norm(f)) < 1e-14
