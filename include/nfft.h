@@ -103,6 +103,9 @@ typedef struct {
                              (non-finite nodes then give unspecified values, never a fault) */
   int precompute;         /* nfft_precompute_strategy (default AUTO); TENSOR is used where a kernel
                              for it exists (D = 1, cell mode) and is ignored elsewhere */
+  int window_points;      /* 0 (default): 2m samples of the truncated window psi_hat;
+                             1: NFFT3's 2m+2 samples of the analytically continued window, same
+                             shape beta and correction; needs m <= 7 and 2m+2 < Ntilde_d */
 } nfft_options;
 
 /* Fills *opt with the defaults above. */

@@ -53,7 +53,7 @@ class Options(ctypes.Structure):
         ("batch", ctypes.c_int64), ("tile", ctypes.c_int64 * 3), ("stream", ctypes.c_void_p),
         ("device", ctypes.c_int), ("method", ctypes.c_int), ("max_subproblem", ctypes.c_int64),
         ("node_begin", ctypes.c_int64), ("node_end", ctypes.c_int64), ("timing", ctypes.c_int),
-        ("check_nodes", ctypes.c_int), ("precompute", ctypes.c_int),
+        ("check_nodes", ctypes.c_int), ("precompute", ctypes.c_int), ("window_points", ctypes.c_int),
     ]
 
 
@@ -126,12 +126,13 @@ class NfftPlan:
     node_range: (begin, end) shard of the plan's SORTED node order (cell order
     in cell mode) processed by forward/adjoint (multi-GPU sharding, DESIGN.md
     §Multi-GPU). precompute: "auto" | "polynomial" | "tensor" (window taps per
-    call vs stored by nfft_precompute).
+    call vs stored by nfft_precompute). window_points: "2m" |
+    "2m+2" (NFFT3's continued-window variant).
     """
 
     def __init__(self, nodes, N, m=4, sigma=2.0, precision="c128", batch=1, tile=None, stream=None,
                  device=None, method="auto", max_subproblem=0, node_range=None, timing=False,
-                 check_nodes=True, precompute="auto"):
+                 check_nodes=True, precompute="auto", window_points="2m"):
         L = lib()
         self.N = tuple(int(n) for n in N)
         self.D = len(self.N)
@@ -166,6 +167,7 @@ class NfftPlan:
         opt.timing = int(bool(timing))
         opt.check_nodes = int(bool(check_nodes))
         opt.precompute = PRECOMPUTE[precompute]
+        opt.window_points = {"2m": 0, "2m+2": 1}[window_points]
         self.opts = opt
         Narr = (ctypes.c_int64 * self.D)(*self.N)
         h = ctypes.c_void_p()

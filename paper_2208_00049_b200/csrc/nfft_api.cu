@@ -51,6 +51,7 @@ struct nfft_plan_s {
   int node_begin = 0, node_end = 0;
   int64_t n_tiles = 1;
   int deg = 14;
+  int m_shape = 0;  // window shape parameter m (the kernels' half-width p->m is m + 1 for 2m+2 points)
   int max_subs = 1;
   int grid_tiled = 1;     // CTAs for the tiled kernels
   int grid_loc = 0;       // CTAs for the conflict-free spread (0: not used)
@@ -202,12 +203,12 @@ template <typename T>
 nfft_status build_window_tables(nfft_plan p) {
   const int n = (int)(p->N[0] + (p->D > 1 ? p->N[1] : 0) + (p->D > 2 ? p->N[2] : 0));
   beta_tensor_kernel<T><<<(n + THREADS - 1) / THREADS, THREADS, 0, p->stream>>>(
-      p->geom, p->beta[0], p->beta[1], p->beta[2], p->d_beta64, (T*)p->d_betaT);
+      p->geom, p->m_shape, p->beta[0], p->beta[1], p->beta[2], p->d_beta64, (T*)p->d_betaT);
   ++p->launches;
   CKL();
   const int nfit = p->D * 2 * p->m;
-  poly_fit_kernel<<<(nfit + 63) / 64, 64, 0, p->stream>>>(p->D, p->m, p->deg + 1, p->beta[0], p->beta[1], p->beta[2],
-                                                          p->d_poly);
+  poly_fit_kernel<<<(nfit + 63) / 64, 64, 0, p->stream>>>(p->D, p->m, p->m_shape, p->m != p->m_shape, p->deg + 1,
+                                                          p->beta[0], p->beta[1], p->beta[2], p->d_poly);
   ++p->launches;
   CKL();
   const size_t cnt = (size_t)nfit * MAX_Z;
@@ -864,6 +865,11 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   *out = nullptr;
   if (D > 3) return NFFT_ERROR_UNSUPPORTED;
   if (D < 1 || M < 1 || m < 1) return NFFT_ERROR_INVALID_VALUE;
+  if (opt_in && (opt_in->window_points < 0 || opt_in->window_points > 1)) return NFFT_ERROR_INVALID_VALUE;
+  // window_points = 1: NFFT3-style 2m+2 samples of the continued window. The kernels then
+  // run with footprint half-width m + 1 while the window SHAPE (beta, scale, correction) keeps m.
+  const int m_shape = m;
+  if (opt_in && opt_in->window_points == 1) m = m + 1;
   if (window != NFFT_WINDOW_KAISER_BESSEL) return NFFT_ERROR_INVALID_VALUE;
   if (precision != NFFT_COMPLEX64 && precision != NFFT_COMPLEX128) return NFFT_ERROR_INVALID_VALUE;
   nfft_options opt;
@@ -942,6 +948,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   p->M = M;
   p->B = opt.batch;
   p->m = m;
+  p->m_shape = m_shape;
   p->sigma = sigma;
   p->prec = precision;
   p->opt = opt;
@@ -960,7 +967,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     p->Nt[d] = Nt[d];
     p->Q[d] = Q[d];
     p->P[d] = P[d];
-    p->beta[d] = M_PI * m * (2.0 - (double)N[d] / (double)Nt[d]);  // reading R4
+    p->beta[d] = M_PI * m_shape * (2.0 - (double)N[d] / (double)Nt[d]);  // reading R4
     n_tiles *= P[d];
   }
   p->n_tiles = n_tiles;

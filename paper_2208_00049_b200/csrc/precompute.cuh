@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(CS_W * 32) cs_scatter_kernel(const R* __restri
 // beta^tensor_{n_d,d} = 1 / (m phi_Base(m n_d / Ntilde_d)), phi_Base(v) = I0(sqrt(beta^2 - (2 pi v)^2))
 // (reading R2). Written in fp64 and in the plan precision.
 template <typename T>
-__global__ void __launch_bounds__(THREADS) beta_tensor_kernel(Geom g, double beta0, double beta1, double beta2,
+__global__ void __launch_bounds__(THREADS) beta_tensor_kernel(Geom g, int ms, double beta0, double beta1, double beta2,
                                                               double* __restrict__ b64, T* __restrict__ bT) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int d = 0, off = i;
@@ -208,10 +208,10 @@ __global__ void __launch_bounds__(THREADS) beta_tensor_kernel(Geom g, double bet
   if (d >= g.D) return;
   const double beta = d == 0 ? beta0 : (d == 1 ? beta1 : beta2);
   const double n = (double)(off - g.N[d] / 2);
-  const double v = (double)g.m * n / (double)g.Nt[d];
+  const double v = (double)ms * n / (double)g.Nt[d];  // ms: window shape m
   const double w = 2.0 * 3.14159265358979323846 * v;
   const double phi = cyl_bessel_i0(sqrt(fma(beta, beta, -w * w)));
-  const double bt = 1.0 / ((double)g.m * phi);
+  const double bt = 1.0 / ((double)ms * phi);
   b64[i] = bt;
   bT[i] = (T)bt;
 }
@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(THREADS) beta_tensor_kernel(Geom g, double bet
 // by least squares on Theta = 2Z equispaced samples (Householder QR in fp64).
 // Samples use the continuous window (limit beta/pi at |u| = 1; R6).
 // One thread per (dimension, tap); out[(d*2m + l)*MAX_Z + z].
-__global__ void poly_fit_kernel(int D, int m, int Z, double beta0, double beta1, double beta2, double* __restrict__ out) {
+__global__ void poly_fit_kernel(int D, int m, int ms, int cont, int Z, double beta0, double beta1, double beta2,
+                                double* __restrict__ out) {
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= D * 2 * m) return;
   const int d = id / (2 * m), l = id % (2 * m);
@@ -236,10 +237,15 @@ __global__ void poly_fit_kernel(int D, int m, int Z, double beta0, double beta1,
       A[r][c] = p;
       p *= zeta;
     }
-    const double u = (zeta + 0.5 + (double)(m - 1 - l)) / (double)m;
+    // m taps per half (the footprint), scale ms (the window shape); cont: the 2m+2 variant samples the
+    // analytic continuation sin(beta s)/(pi s), s = sqrt(u^2 - 1), beyond |u| = 1
+    const double u = (zeta + 0.5 + (double)(m - 1 - l)) / (double)ms;
     const double s2 = 1.0 - u * u;
     double val;
-    if (s2 <= 0.0) {
+    if (s2 < 0.0 && cont) {
+      const double s = sqrt(-s2);
+      val = sin(beta * s) / (3.14159265358979323846 * s);
+    } else if (s2 <= 0.0) {
       val = fabs(u) <= 1.0 ? beta / 3.14159265358979323846 : 0.0;
     } else {
       const double s = sqrt(s2);

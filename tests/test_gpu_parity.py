@@ -497,3 +497,36 @@ def test_batch_adjoint(case):
     plan.close()
     assert "batch" in feats, feats
     _check(w)
+
+
+@pytest.mark.parametrize("case", ["1d_m3", "1d_m7_c64", "2d_m4", "3d_m2", "radial_b32"])
+def test_window_2m_plus_2(case):
+    """NFFT3-style window variant: 2m+2 samples of the continued
+    window, same shape and correction; against the oracle's variant."""
+    if case == "1d_m3":
+        w = workloads.make("cfg1_1d_256", seed=23, m=3)
+    elif case == "1d_m7_c64":
+        w = workloads.make("cfg1_1d_256", seed=24, N=(300,), M=900, m=7)
+        w["precision"] = "c64"
+        w["nodes"] = w["nodes"].astype(np.float32)
+        w["fhat"] = w["fhat"].astype(np.complex64)
+        w["f"] = w["f"].astype(np.complex64)
+    elif case == "2d_m4":
+        w = workloads.make("cfg3_2d_512", seed=25, N=(48, 40), M=2000, m=4)
+    elif case == "3d_m2":
+        w = workloads.make("cfg4_3d_64", seed=26, N=(12, 10, 14), M=800, m=2)
+    else:
+        w = workloads.make("cfg5_radial_s2", seed=27, N=(48, 48), M=1500, m=4, batch=32)
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    plan = _plan(w, window_points="2m+2")
+    fhat = torch.from_numpy(w["fhat"]).cuda()
+    f = torch.from_numpy(w["f"]).cuda()
+    got_f = plan.forward(fhat).cpu().numpy()
+    got_y = plan.adjoint(f).cpu().numpy()
+    plan.close()
+    tol = TOL[w["precision"]]
+    for b in range(w["batch"]):
+        rf = onfft.forward(w["nodes"], w["fhat"][b], w["N"], w["m"], w["sigma"], window_points="2m+2")
+        ry = onfft.adjoint(w["nodes"], w["f"][b], w["N"], w["m"], w["sigma"], window_points="2m+2")
+        assert rel_l2(got_f[b], rf) <= tol and rel_l2(got_y[b], ry) <= tol, (b, rel_l2(got_f[b], rf), rel_l2(got_y[b], ry))
