@@ -216,6 +216,20 @@ nfft_status nfft_get_stage_times(nfft_plan p, int which /* 0 forward, 1 adjoint 
  * (cuFFT's kernels are not counted). */
 nfft_status nfft_get_launch_count(nfft_plan p, int64_t* launches);
 
+/* Online block-size benchmark: the optimisation mode the paper proposes
+ * ("similar to FFTW_MEASURE"; block-size study PAPER.md:729-742).
+ * For each candidate tile (candidates: ncand x D int64, C order; ncand = 0 =
+ * a built-in list per D) a plan is created on `nodes` with *opt (may be NULL)
+ * and that tile, precomputed, and `reps` direct + adjoint transforms
+ * (nfft_execute, zero data, the plan's stream) are timed with CUDA events
+ * after one warm-up. Writes the fastest tile to best_tile[D] and its mean time
+ * per direct + adjoint pair to *best_ms (may be NULL). Candidates whose plan
+ * cannot be created (e.g. tile > Ntilde) are skipped; NFFT_ERROR_INVALID_VALUE
+ * when none is valid. Synchronises; allocates and frees scratch. */
+nfft_status nfft_autotune_tile(int D, const int64_t* N, int64_t M, const void* nodes, double sigma, int m,
+                               nfft_precision precision, const nfft_options* opt, const int64_t* candidates,
+                               int ncand, int reps, int64_t* best_tile, float* best_ms);
+
 /* Paths the plan selected at creation (bit set = in use):
  *   NFFT_FEATURE_CELL_MODE   nodes sorted by cell, cell-mode resampling kernels
  *   NFFT_FEATURE_TENSOR      TENSOR precompute (stored taps)

@@ -27,6 +27,7 @@ NFFT_SYMBOLS = (
     "nfft_precompute", "nfft_forward", "nfft_adjoint", "nfft_plan_destroy", "nfft_status_string",
     "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
     "nfft_get_launch_count", "nfft_run_stage", "nfft_execute", "nfft_get_cell_binning", "nfft_get_features",
+    "nfft_autotune_tile",
 )
 PRECOMPUTE = {"auto": 0, "polynomial": 1, "tensor": 2}
 STAGES = {"precompute": 0, "fwd_deconv": 1, "fwd_fft": 2, "fwd_interp": 3, "adj_spread": 4, "adj_fft": 5,
@@ -87,6 +88,8 @@ def lib():
         "nfft_get_stage_times": [vp, c_int, P(ctypes.c_float)],
         "nfft_get_launch_count": [vp, P(i64)],
         "nfft_get_features": [vp, P(c_int)],
+        "nfft_autotune_tile": [c_int, P(i64), i64, vp, ctypes.c_double, c_int, c_int, vp, P(i64), c_int, c_int,
+                               P(i64), P(ctypes.c_float)],
         "nfft_run_stage": [vp, c_int, vp, vp],
         "nfft_execute": [vp, c_int, vp, vp, vp, vp],
     }
@@ -355,3 +358,34 @@ def nfft_adjoint(nodes, N, f, m=4, sigma=2.0, precision="c128"):
     out = p.adjoint(f)
     p.close()
     return out
+
+
+def autotune_tile(nodes, N, m=4, sigma=2.0, precision="c128", batch=1, candidates=None, reps=5, method="auto"):
+    """Online block-size benchmark (include/nfft.h: nfft_autotune_tile; the
+    FFTW_MEASURE-like mode of PAPER.md:793). candidates: list of D-tuples or
+    None (built-in list). Returns (best_tile, ms per direct + adjoint pair)."""
+    N = tuple(int(n) for n in N)
+    D = len(N)
+    rd = np.float64 if precision == "c128" else np.float32
+    if isinstance(nodes, np.ndarray):
+        nodes = np.ascontiguousarray(nodes.reshape(nodes.shape[0], -1), dtype=rd)
+    else:
+        torch = _torch()
+        nodes = nodes.reshape(nodes.shape[0], -1).to(torch.float64 if precision == "c128" else torch.float32)
+        nodes = nodes.contiguous()
+    opt = Options()
+    lib().nfft_default_options(ctypes.byref(opt))
+    opt.batch = int(batch)
+    opt.method = METHODS[method]
+    cand = None
+    nc = 0
+    if candidates:
+        flat = [int(q) for t in candidates for q in t]
+        cand = (ctypes.c_int64 * len(flat))(*flat)
+        nc = len(candidates)
+    best = (ctypes.c_int64 * D)()
+    ms = ctypes.c_float()
+    _check(lib().nfft_autotune_tile(D, (ctypes.c_int64 * D)(*N), int(nodes.shape[0]), _ptr(nodes), float(sigma), int(m),
+                                    PRECISIONS[precision], ctypes.byref(opt), cand, nc, int(reps), best,
+                                    ctypes.byref(ms)), "nfft_autotune_tile")
+    return tuple(int(q) for q in best), float(ms.value)

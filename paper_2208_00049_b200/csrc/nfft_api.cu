@@ -1140,6 +1140,83 @@ nfft_status nfft_plan_create_ex(nfft_plan* out, int D, const int64_t* N, int64_t
   return create_impl(out, D, N, M, nodes, sigma, m, window, precision, opt);
 }
 
+// Online block-size benchmark (the optimisation mode the paper proposes, "similar to
+// FFTW_MEASURE"; its block-size study): for every candidate tile a plan is built on
+// the caller's nodes, precomputed, and `reps` direct + adjoint transforms (nfft_execute, zero data)
+// are timed with CUDA events after one warm-up; the fastest tile is returned.
+nfft_status nfft_autotune_tile(int D, const int64_t* N, int64_t M, const void* nodes, double sigma, int m,
+                               nfft_precision precision, const nfft_options* opt_in, const int64_t* candidates,
+                               int ncand, int reps, int64_t* best_tile, float* best_ms) {
+  if (D < 1 || D > 3 || !N || !nodes || !best_tile || reps < 1 || ncand < 0 || (ncand > 0 && !candidates))
+    return NFFT_ERROR_INVALID_VALUE;
+  static const int64_t def1[] = {256, 512, 1024, 2048};
+  static const int64_t def2[] = {16, 32, 32, 32, 32, 64, 64, 64, 8, 64};
+  static const int64_t def3[] = {8, 8, 16, 8, 16, 16, 4, 8, 32, 8, 8, 8};
+  const int64_t* cand = candidates;
+  if (ncand == 0) {
+    cand = D == 1 ? def1 : (D == 2 ? def2 : def3);
+    ncand = D == 1 ? 4 : (D == 2 ? 5 : 4);
+  }
+  nfft_options opt;
+  nfft_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  int64_t ncells = 1;
+  for (int d = 0; d < D; ++d) ncells *= N[d];
+  const size_t csz = precision == NFFT_COMPLEX128 ? 16 : 8;
+  const size_t gbytes = (size_t)opt.batch * ncells * csz, nbytes = (size_t)opt.batch * M * csz;
+  void *fhat = nullptr, *fout = nullptr, *fin = nullptr, *yout = nullptr;
+  if (cudaMalloc(&fhat, gbytes) != cudaSuccess || cudaMalloc(&yout, gbytes) != cudaSuccess ||
+      cudaMalloc(&fin, nbytes) != cudaSuccess || cudaMalloc(&fout, nbytes) != cudaSuccess) {
+    cudaFree(fhat);
+    cudaFree(yout);
+    cudaFree(fin);
+    cudaFree(fout);
+    return NFFT_ERROR_OUT_OF_MEMORY;
+  }
+  cudaMemset(fhat, 0, gbytes);
+  cudaMemset(fin, 0, nbytes);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  nfft_status st = NFFT_ERROR_INVALID_VALUE;
+  float best = 0.f;
+  for (int c = 0; c < ncand; ++c) {
+    for (int d = 0; d < 3; ++d) opt.tile[d] = d < D ? cand[(size_t)c * D + d] : 0;
+    nfft_plan p = nullptr;
+    nfft_status s = create_impl(&p, D, N, M, nodes, sigma, m, NFFT_WINDOW_KAISER_BESSEL, precision, &opt);
+    if (s != NFFT_SUCCESS) continue;  // e.g. a tile larger than the grid: skip the candidate
+    s = nfft_execute(p, NFFT_EXEC_PRECOMPUTE | NFFT_EXEC_FORWARD | NFFT_EXEC_ADJOINT, fhat, fout, fin, yout);
+    float ms = 0.f;
+    if (s == NFFT_SUCCESS) {
+      cudaEventRecord(e0, p->stream);
+      for (int r = 0; r < reps && s == NFFT_SUCCESS; ++r)
+        s = nfft_execute(p, NFFT_EXEC_FORWARD | NFFT_EXEC_ADJOINT, fhat, fout, fin, yout);
+      cudaEventRecord(e1, p->stream);
+      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess)
+        s = NFFT_ERROR_CUDA;
+    }
+    nfft_plan_destroy(p);
+    if (s != NFFT_SUCCESS) {
+      st = s;
+      break;
+    }
+    ms /= reps;
+    if (st != NFFT_SUCCESS || ms < best) {
+      best = ms;
+      for (int d = 0; d < D; ++d) best_tile[d] = cand[(size_t)c * D + d];
+      st = NFFT_SUCCESS;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(fhat);
+  cudaFree(yout);
+  cudaFree(fin);
+  cudaFree(fout);
+  if (st == NFFT_SUCCESS && best_ms) *best_ms = best;
+  return st;
+}
+
 nfft_status nfft_set_nodes(nfft_plan p, const void* nodes) {
   if (!p || !nodes) return NFFT_ERROR_INVALID_VALUE;
   DeviceGuard guard(p->device);

@@ -548,3 +548,16 @@ def test_very_dense_cell(D):
     np.testing.assert_array_equal(cb[0], ref_perm)
     np.testing.assert_array_equal(cb[1], ref_offs)
     _check(w)
+
+
+@pytest.mark.parametrize("D", [1, 2, 3])
+def test_autotune_tile(D):
+    """Online block-size benchmark: returns one of the candidates
+    with a positive time; a plan with that tile matches the oracle."""
+    import paper_2208_00049_b200 as pkg
+    N = {1: (512,), 2: (64, 48), 3: (16, 12, 10)}[D]
+    cand = {1: [(64,), (128,), (512,)], 2: [(16, 16), (32, 32), (16, 32)], 3: [(4, 4, 8), (8, 8, 8)]}[D]
+    w = workloads.make({1: "cfg1_1d_256", 2: "cfg3_2d_512", 3: "cfg4_3d_64"}[D], seed=40 + D, N=N, M=2000, m=3)
+    tile, ms = pkg.autotune_tile(w["nodes"], w["N"], m=3, candidates=cand, reps=3)
+    assert tile in cand and ms > 0, (tile, ms)
+    _check(w, tile=tile)
