@@ -171,9 +171,15 @@ nfft_status nfft_run_stage(nfft_plan p, int stage, const void* in, void* out);
  * overlaps the direct NFFT's deconvolution + FFT, and the adjoint (separate
  * scratch grid and cuFFT plan) overlaps the direct NFFT. The direct NFFT maps
  * fhat_grid -> f_nodes and the adjoint maps the INDEPENDENT input f_in ->
- * y_grid (f_in must not be the f_nodes of the same call). Device pointers only.
- * All work is forked from and joined back into the plan stream (stream order
- * and CUDA-graph capture are as for one stream-ordered call). No node check.
+ * y_grid (f_in must not be the f_nodes of the same call). Each data pointer
+ * may be device or host memory: host inputs are uploaded and host outputs
+ * downloaded on the stream of their own chain (so the direct NFFT's copies
+ * overlap the adjoint's), through plan-owned staging buffers; the call does
+ * NOT synchronise, host outputs are valid once the plan stream has (use
+ * pinned host memory for asynchronous copies). All work is forked from and
+ * joined back into the plan stream (stream order and CUDA-graph capture are as
+ * for one stream-ordered call; graph capture needs device pointers). No node
+ * check.
  */
 typedef enum { NFFT_EXEC_PRECOMPUTE = 1, NFFT_EXEC_FORWARD = 2, NFFT_EXEC_ADJOINT = 4 } nfft_exec_flags;
 nfft_status nfft_execute(nfft_plan p, int flags, const void* fhat_grid, void* f_nodes, const void* f_in,

@@ -114,7 +114,9 @@ struct nfft_plan_s {
   void* d_betaT = nullptr;
   double* d_poly = nullptr;  // D*2m*MAX_Z
   void* d_stage_grid = nullptr;   // B * prod N complex (host-pointer staging)
-  void* d_stage_nodes = nullptr;  // B * M complex
+  void* d_stage_nodes = nullptr;
+  void* d_stage_nodes2 = nullptr;  // nfft_execute: the adjoint chain's host-input staging
+  void* d_stage_grid2 = nullptr;   // nfft_execute: the adjoint chain's host-output staging
   cufftHandle fft = 0;      // forward: out-of-place grid_in -> grid
   bool fft_ok = false;
   cufftHandle fft_adj = 0;  // adjoint: in place on grid_adj (own plan: may run concurrently)
@@ -178,7 +180,7 @@ bool is_device_pointer(const void* p) {
 
 void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
-                  p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_cnt, p->d_tile_total,
+                  p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_stage_nodes2, p->d_stage_grid2, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
                   p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT};
   for (void* b : bufs)
@@ -817,6 +819,28 @@ template <typename T>
 nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, const void* f_in, void* y_out) {
   using C = typename cplx<T>::type;
   const bool pre = flags & NFFT_EXEC_PRECOMPUTE, fwd = flags & NFFT_EXEC_FORWARD, adj = flags & NFFT_EXEC_ADJOINT;
+  // host pointers: staging buffers per chain (the chains run concurrently)
+  const size_t gbytes = (size_t)p->B * p->geom.ngrid_cells * sizeof(C), nbytes = (size_t)p->B * p->M * sizeof(C);
+  const bool h_fhat = fwd && !is_device_pointer(fhat), h_fout = fwd && !is_device_pointer(f_out);
+  const bool h_fin = adj && !is_device_pointer(f_in), h_y = adj && !is_device_pointer(y_out);
+  void* host_fout = nullptr;
+  void* host_y = nullptr;
+  if (h_fhat) {
+    if (!p->d_stage_grid) CK(cudaMalloc(&p->d_stage_grid, gbytes));
+  }
+  if (h_fout) {
+    if (!p->d_stage_nodes) CK(cudaMalloc(&p->d_stage_nodes, nbytes));
+    host_fout = f_out;
+    f_out = p->d_stage_nodes;
+  }
+  if (h_fin) {
+    if (!p->d_stage_nodes2) CK(cudaMalloc(&p->d_stage_nodes2, nbytes));
+  }
+  if (h_y) {
+    if (!p->d_stage_grid2) CK(cudaMalloc(&p->d_stage_grid2, gbytes));
+    host_y = y_out;
+    y_out = p->d_stage_grid2;
+  }
   CK(cudaEventRecord(p->ev_fork, p->stream));
   if (pre) {
     CK(cudaStreamWaitEvent(p->side_pre, p->ev_fork, 0));
@@ -825,17 +849,27 @@ nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, 
   }
   if (adj) {
     CK(cudaStreamWaitEvent(p->side_adj, p->ev_fork, 0));
+    if (h_fin) {
+      CK(cudaMemcpyAsync(p->d_stage_nodes2, f_in, nbytes, cudaMemcpyHostToDevice, p->side_adj));
+      f_in = p->d_stage_nodes2;
+    }
     if (pre) CK(cudaStreamWaitEvent(p->side_adj, p->ev_pre, 0));
     TRY(stage_spread<T>(p, (const C*)f_in, p->side_adj));
     TRY(stage_fft<T>(p, CUFFT_INVERSE, p->side_adj));
     TRY(stage_crop<T>(p, (C*)y_out, p->side_adj));
+    if (h_y) CK(cudaMemcpyAsync(host_y, y_out, gbytes, cudaMemcpyDeviceToHost, p->side_adj));
     CK(cudaEventRecord(p->ev_adj, p->side_adj));
   }
   if (fwd) {
+    if (h_fhat) {
+      CK(cudaMemcpyAsync(p->d_stage_grid, fhat, gbytes, cudaMemcpyHostToDevice, p->stream));
+      fhat = p->d_stage_grid;
+    }
     TRY(stage_deconv<T>(p, (const C*)fhat, p->stream));
     TRY(stage_fft<T>(p, CUFFT_FORWARD, p->stream));
     if (pre) CK(cudaStreamWaitEvent(p->stream, p->ev_pre, 0));
     TRY(stage_interp<T>(p, (C*)f_out, p->stream));
+    if (h_fout) CK(cudaMemcpyAsync(host_fout, f_out, nbytes, cudaMemcpyDeviceToHost, p->stream));
   }
   if (pre) CK(cudaStreamWaitEvent(p->stream, p->ev_pre, 0));
   if (adj) CK(cudaStreamWaitEvent(p->stream, p->ev_adj, 0));
@@ -1279,10 +1313,8 @@ nfft_status nfft_execute(nfft_plan p, int flags, const void* fhat_grid, void* f_
                          void* y_grid) {
   if (!p || flags <= 0 || flags > 7) return NFFT_ERROR_INVALID_VALUE;
   const bool fwd = flags & NFFT_EXEC_FORWARD, adj = flags & NFFT_EXEC_ADJOINT;
-  if (fwd && (!fhat_grid || !f_nodes || !is_device_pointer(fhat_grid) || !is_device_pointer(f_nodes)))
-    return NFFT_ERROR_INVALID_VALUE;
-  if (adj && (!f_in || !y_grid || !is_device_pointer(f_in) || !is_device_pointer(y_grid)))
-    return NFFT_ERROR_INVALID_VALUE;
+  if (fwd && (!fhat_grid || !f_nodes)) return NFFT_ERROR_INVALID_VALUE;
+  if (adj && (!f_in || !y_grid)) return NFFT_ERROR_INVALID_VALUE;
   if (!(flags & NFFT_EXEC_PRECOMPUTE) && !p->precomputed) return NFFT_ERROR_NOT_PRECOMPUTED;
   DeviceGuard guard(p->device);
   nfft_status s = p->prec == NFFT_COMPLEX128 ? execute_impl<double>(p, flags, fhat_grid, f_nodes, f_in, y_grid)
