@@ -90,6 +90,7 @@ struct nfft_plan_s {
   bool tile_binned = false;  // cell mode: perm/offsets (tile sort) computed on demand for nfft_get_binning
   int64_t ncells = 0;        // prod Ntilde
   size_t r1_spread_bytes = 0;
+  int s1_occ = 1;            // spread1c CTAs resident per SM
   size_t sc_bytes = 0;       // spread_cell shared memory
   int sc_cap = 0;            // spread_cell node slots per chunk
   void* d_kc = nullptr;      // D*M reals: coordinates in cell order (SoA)
@@ -336,6 +337,7 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
                cudaSuccess &&
            occ_s >= 1;
       p->r1_spread_bytes = sb;
+      p->s1_occ = occ_s;
     }
     if (p->D >= 2 && ks.interp_cell && ks.spread_cell) {
       int wrows = 1;
@@ -615,7 +617,9 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
   } else if (p->cellmode && p->D == 1) {
     const int sharded = p->node_begin > 0 || p->node_end < p->M;
-    ks.interp1<<<(unsigned)((p->M + I1_THREADS - 1) / I1_THREADS), I1_THREADS, 0, st>>>(
+    static const int i1_ctas = getenv("NFFTB_I1_CTAS") ? atoi(getenv("NFFTB_I1_CTAS")) : 0;  // diagnostic
+    const unsigned gi = (unsigned)((p->M + I1_THREADS - 1) / I1_THREADS);
+    ks.interp1<<<i1_ctas > 0 ? std::min<unsigned>(gi, (unsigned)i1_ctas) : gi, I1_THREADS, 0, st>>>(
         p->geom, wp, grid, (const T*)p->d_kc, p->d_jc, p->node_begin, p->node_end, sharded, f);
   } else if (p->tiled) {
     ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
@@ -671,7 +675,13 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     rec(p, 1, 1);
     const int sharded = p->node_begin > 0 || p->node_end < p->M;
     const int segs = (int)((p->Nt[0] + S1_SEG - 1) / S1_SEG);
-    ks.spread1<<<(unsigned)((segs + S1_WARPS - 1) / S1_WARPS), 32 * S1_WARPS, p->r1_spread_bytes, st>>>(
+    // one resident wave, grid-stride over the segments: measured 56.5 -> 49.4 us per execute step (1D
+    // config 2), because the full-size grid kept every SM's shared memory busy and left no room for the
+    // concurrent direct NFFT's kernels; NFFTB_S1_CTAS overrides (diagnostic)
+    static const int s1_ctas = getenv("NFFTB_S1_CTAS") ? atoi(getenv("NFFTB_S1_CTAS")) : 0;
+    const unsigned gs = (unsigned)((segs + S1_WARPS - 1) / S1_WARPS);
+    const unsigned cap = s1_ctas > 0 ? (unsigned)s1_ctas : (unsigned)(p->sm_count * std::max(1, p->s1_occ));
+    ks.spread1<<<std::min<unsigned>(gs, cap), 32 * S1_WARPS, p->r1_spread_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_kc, p->d_jc, p->d_cstart, p->node_begin, p->node_end, sharded, grid);
     ++p->launches;
     CKL();

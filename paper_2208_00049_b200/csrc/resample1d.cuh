@@ -43,9 +43,8 @@ __global__ void __launch_bounds__(I1_THREADS) interp1c_kernel(Geom g, WinPoly<T>
                                                               int nb, int ne, int sharded,
                                                               typename cplx<T>::type* __restrict__ f) {
   using C = typename cplx<T>::type;
-  const int pc = blockIdx.x * I1_THREADS + threadIdx.x;
-  if (pc >= g.M) return;
-  if (sharded && (pc < nb || pc >= ne)) return;  // shard = range of the cell-sorted order
+  for (int pc = blockIdx.x * I1_THREADS + threadIdx.x; pc < g.M; pc += gridDim.x * I1_THREADS) {
+  if (sharded && (pc < nb || pc >= ne)) continue;  // shard = range of the cell-sorted order
   const int j = jc[pc];
   double frac;
   const int Nt = g.Nt[0];
@@ -79,6 +78,7 @@ __global__ void __launch_bounds__(I1_THREADS) interp1c_kernel(Geom g, WinPoly<T>
     }
     f[(long long)b * g.M + j] = acc;
   }
+  }  // nodes
 }
 
 // ---------------------------------------------------------------- adjoint
@@ -126,8 +126,10 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Nt = g.Nt[0];
-  const int y0 = (blockIdx.x * S1_WARPS + warp) * S1_SEG;
-  if (y0 >= Nt) return;
+  // grid-stride over the warp segments (the launch may use fewer CTAs than segments)
+  for (int wseg = blockIdx.x * S1_WARPS + warp;; wseg += gridDim.x * S1_WARPS) {
+  const int y0 = wseg * S1_SEG;
+  if (y0 >= Nt) break;
   const int nseg = min(S1_SEG, Nt - y0);
   const int NE = nseg + 2 * M - 1;  // window cell e <-> binning cell (y0 - m + e) mod Nt
   unsigned char* wb = smem_raw + (size_t)warp * s1_warp_bytes(M, sizeof(C), sizeof(T));
@@ -274,6 +276,7 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
     }
     __syncwarp();
   }
+  }  // segments
 }
 
 // ---------------------------------------------------------------- TENSOR precompute (D = 1)
