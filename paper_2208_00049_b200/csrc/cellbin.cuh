@@ -214,6 +214,20 @@ __global__ void __launch_bounds__(CL_THREADS) cl_fix_kernel(Geom g, const int* _
   for (int c = blockIdx.x * CL_THREADS + threadIdx.x; c < ncells; c += gridDim.x * CL_THREADS) {
     const int a = cstart[c], n = cstart[c + 1] - a;
     if (n < 2 || n > CL_SMALL) continue;
+    if (n == 2) {  // the common case (~80% of the multi-node cells of a uniform set): one compare-swap
+      const int j0 = jc[a], j1 = jc[a + 1];
+      if (j0 > j1) {
+        jc[a] = j1;
+        jc[a + 1] = j0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const R k0 = kc[(long long)d * g.M + a], k1 = kc[(long long)d * g.M + a + 1];
+          kc[(long long)d * g.M + a] = k1;
+          kc[(long long)d * g.M + a + 1] = k0;
+        }
+      }
+      continue;
+    }
     int jv[CL_SMALL];
     R kv[CL_SMALL][D];
 #pragma unroll
