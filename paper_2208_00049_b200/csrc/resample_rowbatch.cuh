@@ -30,7 +30,7 @@ namespace nfftb {
 constexpr int RB_THREADS = 256;  // 8 warps
 constexpr int RB_LANES = 32;     // vectors per chunk
 constexpr int RB_SEG = 16;       // cells per CTA (last dimension)
-constexpr int RB_U = 4;          // nodes per warp step (loads in flight together)
+constexpr int RB_U = 2;          // nodes per warp step (loads in flight together)
 
 // (B, M) -> (M, BP) and back; BP = batch padded to a multiple of 32 (pad rows unused)
 template <typename T>
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) taps_nd_kernel(Geom g, WinPoly<T> wp, con
 }
 
 template <typename T, int M>
-__global__ void __launch_bounds__(RB_THREADS) spread_rowbatch_kernel(Geom g, const typename cplx<T>::type* __restrict__ fT,
+__global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 3 : 2) spread_rowbatch_kernel(Geom g, const typename cplx<T>::type* __restrict__ fT,
                                                                      int BP, const T* __restrict__ kc,
                                                                      const T* __restrict__ wt,
                                                                      const int* __restrict__ jc,
