@@ -65,15 +65,16 @@ __global__ void __launch_bounds__(CL_THREADS) cl_count_kernel(const R* __restric
                                                               int* __restrict__ err,
                                                               unsigned long long* __restrict__ status, int ntiles,
                                                               int* __restrict__ ctr) {
-  const int j = blockIdx.x * CL_THREADS + threadIdx.x;
-  if (j < ntiles) status[j] = 0ull;  // scan state of this precompute (read only by cl_scan)
-  if (j < 4) ctr[j] = 0;             // [0] scan ticket, [2] fix-list length
-  if (j >= g.M) return;
-  R k[MAX_D];
-  bool bad;
-  const int c = cell_key<R, D>(nodes, g, j, k, bad);
-  if (bad) atomicOr(err, 1);
-  slot[j] = atomicAdd(count + c, 1);
+  const int t0 = blockIdx.x * CL_THREADS + threadIdx.x, stride = gridDim.x * CL_THREADS;
+  for (int j = t0; j < ntiles; j += stride) status[j] = 0ull;  // scan state (read only by cl_scan)
+  if (t0 < 4) ctr[t0] = 0;  // [0] scan ticket, [2] fix-list length
+  for (int j = t0; j < g.M; j += stride) {  // grid-stride: the launch may use fewer threads than nodes
+    R k[MAX_D];
+    bool bad;
+    const int c = cell_key<R, D>(nodes, g, j, k, bad);
+    if (bad) atomicOr(err, 1);
+    slot[j] = atomicAdd(count + c, 1);
+  }
 }
 
 // One-pass exclusive scan with decoupled look-back. cstart[n] = total.
@@ -172,8 +173,8 @@ __global__ void __launch_bounds__(CL_THREADS) cl_place_kernel(const R* __restric
                                                               const int* __restrict__ cstart,
                                                               R* __restrict__ kc, int* __restrict__ jc,
                                                               int* __restrict__ ctr, int* __restrict__ fixl) {
-  const int j = blockIdx.x * CL_THREADS + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  for (int j = blockIdx.x * CL_THREADS + threadIdx.x; j - lane < g.M; j += gridDim.x * CL_THREADS) {
   bool listed = false;
   int c = 0;
   if (j < g.M) {
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(CL_THREADS) cl_place_kernel(const R* __restric
     b0 = __shfl_sync(0xffffffffu, b0, __ffs(mb) - 1);
     if (listed) fixl[b0 + __popc(mb & lt)] = c;
   }
+  }  // nodes
 }
 
 // Stable order (node index) inside every cell with >= 2 nodes. Cells with

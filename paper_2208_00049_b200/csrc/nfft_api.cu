@@ -511,8 +511,14 @@ nfft_status cell_sort_d(nfft_plan p, cudaStream_t st) {
   const int M = (int)p->M;
   const int nc = (int)p->ncells;
   const int ntiles = (nc + CL_SCAN_TILE - 1) / CL_SCAN_TILE;
-  const unsigned gm = (unsigned)((std::max(M, ntiles) + CL_THREADS - 1) / CL_THREADS);
-  const unsigned gp = (unsigned)((M + CL_THREADS - 1) / CL_THREADS);
+  // NFFTB_PRE_CTAS caps the node-parallel kernels' grids (grid-stride; diagnostic)
+  static const int pre_ctas = getenv("NFFTB_PRE_CTAS") ? atoi(getenv("NFFTB_PRE_CTAS")) : 0;
+  unsigned gm = (unsigned)((std::max(M, ntiles) + CL_THREADS - 1) / CL_THREADS);
+  unsigned gp = (unsigned)((M + CL_THREADS - 1) / CL_THREADS);
+  if (pre_ctas > 0) {
+    gm = std::min<unsigned>(gm, (unsigned)pre_ctas);
+    gp = std::min<unsigned>(gp, (unsigned)pre_ctas);
+  }
   static const int stop = getenv("NFFTB_DIAG_PRE_STOP") ? atoi(getenv("NFFTB_DIAG_PRE_STOP")) : 4;  // diagnostic
   if (stop < 1) return NFFT_SUCCESS;
   cl_count_kernel<R, D><<<gm, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_ccount, p->d_cslot, p->d_err,
@@ -524,7 +530,8 @@ nfft_status cell_sort_d(nfft_plan p, cudaStream_t st) {
   cl_place_kernel<R, D><<<gp, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_cslot, p->d_cstart,
                                                    (R*)p->d_kc, p->d_jc, p->d_ctr, p->d_big);
   if (stop < 4) return NFFT_SUCCESS;
-  const unsigned gf = (unsigned)std::min<int64_t>((nc + CL_THREADS - 1) / CL_THREADS, p->sm_count * 8);
+  const unsigned gf = (unsigned)std::min<int64_t>((nc + CL_THREADS - 1) / CL_THREADS,
+                                                  pre_ctas > 0 ? pre_ctas : p->sm_count * 8);
   cl_fix_kernel<R, D><<<gf, CL_THREADS, 0, st>>>(p->geom, p->d_cstart, (R*)p->d_kc, p->d_jc, nc, p->d_ctr, p->d_big,
                                                  p->d_cslot, (R*)p->d_ks);
   p->launches += 4;
@@ -886,9 +893,9 @@ nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, 
   return NFFT_SUCCESS;
 }
 
-// nfft_execute: the adjoint chain (spread -> FFT -> crop) is the longer one, so its internal
-// stream gets the highest priority (its CTAs are scheduled first when both chains compete);
-// NFFTB_ADJ_PRIORITY=0 keeps the default priority (diagnostic).
+// nfft_execute: the precompute and the adjoint chain (spread -> FFT -> crop) form the critical
+// path, so their internal streams get the highest priority (their CTAs are scheduled first when
+// they compete with the direct NFFT); NFFTB_ADJ_PRIORITY=0 keeps the default priority (diagnostic).
 static int adj_priority() {
   int lo = 0, hi = 0;
   if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return 0;
@@ -1123,7 +1130,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
       CUFFT_SUCCESS)
     return fail(NFFT_ERROR_CUFFT);
   p->fft_adj_ok = true;
-  if (cudaStreamCreateWithFlags(&p->side_pre, cudaStreamNonBlocking) != cudaSuccess ||
+  if (cudaStreamCreateWithPriority(&p->side_pre, cudaStreamNonBlocking, adj_priority()) != cudaSuccess ||
       cudaStreamCreateWithPriority(&p->side_adj, cudaStreamNonBlocking, adj_priority()) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_pre, cudaEventDisableTiming) != cudaSuccess ||
