@@ -586,3 +586,20 @@ def test_execute_with_host_buffers(config):
         for b in range(w["batch"]):
             assert rel_l2(fout[b], rf[b]) <= 1e-12 and rel_l2(yout[b], ry[b]) <= 1e-12
     plan.close()
+
+
+@pytest.mark.parametrize("case", ["3d", "2d_batch8"])
+def test_seam_and_out_of_range_nodes(case):
+    """Nodes on the torus seam (k = +-1/2), exactly on grid points, far outside
+    [-1/2, 1/2) (periodic fold) and coincident, through the default cell-mode
+    kernels (3D; the 2D batch adjoint with B = 8)."""
+    rng = np.random.default_rng(60)
+    D = 3 if case == "3d" else 2
+    special = np.array([[0.5] * D, [-0.5] * D, [1.75] * D, [-2.3] * D, [0.0] * D, [0.0] * D,
+                        [0.25, -0.5, 0.5][:D], [0.5 - 1e-16, 0.125, -0.375][:D]])
+    nodes = np.concatenate([special, rng.random((600, D)) - 0.5])
+    N = (12, 10, 16) if D == 3 else (40, 32)
+    B = 1 if D == 3 else 8
+    w = dict(nodes=nodes, N=N, m=3, sigma=2.0, precision="c128", batch=B,
+             fhat=workloads.complex_normal(rng, (B,) + N), f=workloads.complex_normal(rng, (B, len(nodes))))
+    _check(w)
