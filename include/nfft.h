@@ -239,10 +239,12 @@ nfft_status nfft_autotune_tile(int D, const int64_t* N, int64_t M, const void* n
 /* Paths the plan selected at creation (bit set = in use):
  *   NFFT_FEATURE_CELL_MODE   nodes sorted by cell, cell-mode resampling kernels
  *   NFFT_FEATURE_TENSOR      TENSOR precompute (stored taps)
- *   NFFT_FEATURE_BATCH       2D batch adjoint: row segments, lanes = batch vectors (B >= 8) */
+ *   NFFT_FEATURE_BATCH       2D batch adjoint: row segments, lanes = batch vectors (B >= 8)
+ *   NFFT_FEATURE_WBLOCK      D = 2, 3 adjoint over warp-owned cell blocks and stored taps */
 #define NFFT_FEATURE_CELL_MODE 1
 #define NFFT_FEATURE_TENSOR 4
 #define NFFT_FEATURE_BATCH 8
+#define NFFT_FEATURE_WBLOCK 16
 nfft_status nfft_get_features(nfft_plan p, int* features);
 
 #ifdef __cplusplus

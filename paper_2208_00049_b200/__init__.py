@@ -322,10 +322,10 @@ class NfftPlan:
         return dict(deconv=ms[0], fft=ms[1], resample=ms[2], zero=ms[3], precompute=ms[4])
 
     def features(self):
-        """Paths in use: {"cell_mode", "tensor", "batch"} (include/nfft.h: nfft_get_features)."""
+        """Paths in use: {"cell_mode", "tensor", "batch", "wblock"} (include/nfft.h: nfft_get_features)."""
         v = ctypes.c_int()
         _check(lib().nfft_get_features(self._h, ctypes.byref(v)), "nfft_get_features")
-        return {k for k, bit in (("cell_mode", 1), ("tensor", 4), ("batch", 8)) if v.value & bit}
+        return {k for k, bit in (("cell_mode", 1), ("tensor", 4), ("batch", 8), ("wblock", 16)) if v.value & bit}
 
     def launches(self):
         n = ctypes.c_int64()

@@ -32,7 +32,10 @@ struct KernelSet {
   void (*spread_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
   // D = 2 batches: row-segment spread, lanes = batch vectors (resample_rowbatch.cuh)
   void (*spread_rowbatch)(Geom, const C*, int, const T*, const T*, const int*, const int*, C*);
-  void (*taps_nd)(Geom, WinPoly<T>, const T*, T*);
+  void (*taps_nd)(Geom, WinPoly<T>, const T*, T*, int*);
+  // D = 2, 3: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
+  void (*spread_wb)(Geom, const C*, const int*, const T*, const int*, C*);
+  size_t wb_warp_bytes;
 };
 
 template <typename T> KernelSet<T> kernels_d1(int m);
@@ -54,6 +57,7 @@ inline KernelSet<T> kernels_for(int D, int m) {
 #include "resample_nd.cuh"
 #include "resample_cell.cuh"
 #include "resample_rowbatch.cuh"
+#include "resample_wblock.cuh"
 namespace nfftb {
 template <typename T, int D, int M>
 KernelSet<T> make_set() {
@@ -61,7 +65,7 @@ KernelSet<T> make_set() {
   KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
                  interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
                  spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                 nullptr, nullptr, nullptr, nullptr};
+                 nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if constexpr (D == 1) {
     k.interp1 = interp1c_kernel<T, M, DEG>;
     k.spread1 = spread1c_kernel<T, M, DEG>;
@@ -73,6 +77,8 @@ KernelSet<T> make_set() {
     k.spread_cell = spread_cell_kernel<T, D, M, DEG>;
     if constexpr (D == 2) k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
     k.taps_nd = taps_nd_kernel<T, D, M, DEG>;
+    k.spread_wb = spread_wb_kernel<T, D, M>;
+    k.wb_warp_bytes = WbCfg<T, D, M>::WARP_BYTES;
   }
   if constexpr (D <= 2) {
     k.spread_loc = spread_loc_kernel<T, D, M, DEG>;

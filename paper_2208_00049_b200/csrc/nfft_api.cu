@@ -27,6 +27,7 @@
 #include "resample_nd.cuh"
 #include "resample_cell.cuh"
 #include "resample_rowbatch.cuh"
+#include "resample_wblock.cuh"
 
 using namespace nfftb;
 
@@ -99,6 +100,10 @@ struct nfft_plan_s {
   int bp = 0;                // batch padded to a multiple of 32
   void* d_fT = nullptr;      // M * bp complex: node values, transposed (node-major)
   size_t rb_bytes = 0;
+  bool wbmode = false;       // D = 2, 3 cell mode: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
+  size_t wb_bytes = 0;
+  void* d_fc = nullptr;      // B * M complex: node values in cell order (warp-block adjoint)
+  int* d_cl = nullptr;       // M: last-dimension cell of every cell-sorted position
 
   void* d_wt = nullptr;      // M * 2m reals: taps of every cell-sorted position
   int* d_jc = nullptr;       // M: node index of every cell-sorted position
@@ -183,7 +188,7 @@ void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_stage_nodes2, p->d_stage_grid2, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
-                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT};
+                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT, p->d_fc, p->d_cl};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -386,6 +391,20 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
     p->batchmode = ok;
   }
+  if (p->wbmode) {
+    bool ok = p->cellmode && !p->batchmode && ks.spread_wb;
+    if (ok) {
+      p->wb_bytes = (size_t)WB_WARPS * ks.wb_warp_bytes;
+      int o = 0;
+      ok = cudaFuncSetAttribute((const void*)ks.spread_wb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->wb_bytes) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void*)ks.spread_wb, 32 * WB_WARPS, p->wb_bytes) ==
+               cudaSuccess &&
+           o >= 1;
+      cudaGetLastError();
+    }
+    p->wbmode = ok;
+  }
   p->use_ind = false;
   if (p->D >= 2 && !p->cellmode && p->tiled && ks.interp_nd &&
       (p->opt.method == NFFT_METHOD_AUTO || p->opt.method == NFFT_METHOD_TILED)) {
@@ -553,10 +572,10 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
   if (p->cellmode) {
     TRY(cell_sort<R>(p, st));
     p->tile_binned = false;
-    if (p->batchmode) {  // taps of every node for the batch adjoint (TENSOR layout)
+    if (p->batchmode || p->wbmode) {  // taps of every node for the D >= 2 adjoint (TENSOR layout)
       const KernelSet<R>& ks = kernels_of<R>(p);
-      ks.taps_nd<<<(unsigned)((p->M + 255) / 256), 256, 0, st>>>(p->geom, poly_of<R>(p), (const R*)p->d_kc,
-                                                                 (R*)p->d_wt);
+      ks.taps_nd<<<(unsigned)((p->M + TN_NODES - 1) / TN_NODES), TN_NODES, 0, st>>>(p->geom, poly_of<R>(p), (const R*)p->d_kc,
+                                                                 (R*)p->d_wt, p->wbmode ? p->d_cl : nullptr);
       ++p->launches;
       CKL();
     }
@@ -654,6 +673,22 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     const unsigned segs = (unsigned)(p->Nt[0] * ((p->Nt[1] + RB_SEG - 1) / RB_SEG));
     ks.spread_rowbatch<<<dim3(segs, nch), RB_THREADS, p->rb_bytes, st>>>(
         p->geom, (const C*)p->d_fT, p->bp, (const T*)p->d_kc, (const T*)p->d_wt, p->d_jc, p->d_cstart, grid);
+    p->launches += 2;
+    CKL();
+    return NFFT_SUCCESS;
+  }
+  if (p->wbmode) {
+    // node values in cell order, then owner-computes per warp block: every grid cell written exactly
+    // once, no zero pass
+    rec(p, 1, 1);
+    using C = typename cplx<T>::type;
+    permute_f_kernel<T><<<dim3((unsigned)((p->M + 255) / 256), (unsigned)p->B), 256, 0, st>>>(
+        f, p->d_jc, (int)p->M, p->node_begin, p->node_end, (C*)p->d_fc);
+    long long nblk = (p->Nt[0] + WB_K0 - 1) / WB_K0;
+    if (p->D == 3) nblk *= (p->Nt[1] + 3) / 4 * ((p->Nt[2] + 7) / 8);
+    else nblk *= (p->Nt[1] + 31) / 32;
+    ks.spread_wb<<<dim3((unsigned)((nblk + WB_WARPS - 1) / WB_WARPS), (unsigned)p->B), 32 * WB_WARPS, p->wb_bytes, st>>>(
+        p->geom, (const C*)p->d_fc, p->d_cl, (const T*)p->d_wt, p->d_cstart, grid);
     p->launches += 2;
     CKL();
     return NFFT_SUCCESS;
@@ -1094,6 +1129,13 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   p->bp = (int)((p->B + 31) / 32 * 32);
   if (ok && p->batchmode)
     ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && alloc(&p->d_wt, (size_t)M * D * 2 * m * rs);
+  // D = 2, 3 (not batched): warp-block adjoint over the TENSOR taps; the last-dimension window
+  // (32 or 8 lanes + 2m - 1 cells) must not wrap onto itself
+  p->wbmode = p->cellmode && !p->batchmode && D >= 2 && Nt[D - 1] >= (D == 3 ? 8 : 32) + 2 * m - 1 &&
+              !getenv("NFFTB_NO_WB");
+  if (ok && p->wbmode)
+    ok = alloc(&p->d_wt, (size_t)M * D * 2 * m * rs) && alloc(&p->d_fc, (size_t)M * p->B * csz) &&
+         alloc((void**)&p->d_cl, (size_t)M * 4);
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
   {
     const int bytes = (int)(n_tiles * 4);
@@ -1471,7 +1513,7 @@ nfft_status nfft_get_stage_times(nfft_plan p, int which, float* ms) {
 nfft_status nfft_get_features(nfft_plan p, int* features) {
   if (!p || !features) return NFFT_ERROR_INVALID_VALUE;
   *features = (p->cellmode ? NFFT_FEATURE_CELL_MODE : 0) | (p->tensor ? NFFT_FEATURE_TENSOR : 0) |
-              (p->batchmode ? NFFT_FEATURE_BATCH : 0);
+              (p->batchmode ? NFFT_FEATURE_BATCH : 0) | (p->wbmode ? NFFT_FEATURE_WBLOCK : 0);
   return NFFT_SUCCESS;
 }
 

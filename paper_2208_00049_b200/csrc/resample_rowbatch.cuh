@@ -81,20 +81,37 @@ __host__ __device__ inline size_t rb_smem_bytes(int M, int rsize) {
 }
 
 // Taps of every cell-sorted node, wt[pos][d][t] (the paper's TENSOR layout,
-// PAPER.md:599-604), computed by nfft_precompute for the batch adjoint.
+// PAPER.md:599-604), computed by nfft_precompute for the D >= 2 adjoints. A CTA
+// of TN_NODES threads (one node each) builds its contiguous block of the table
+// in shared memory (row stride D * 2m + 1: conflict-free) and writes it out
+// coalesced (the per-thread 8-byte stores at a D * 2m stride were store-bound).
+// cl (optional): the last-dimension binning cell of every position.
+constexpr int TN_NODES = 64;
 template <typename T, int D, int M, int DEG>
-__global__ void __launch_bounds__(256) taps_nd_kernel(Geom g, WinPoly<T> wp, const T* __restrict__ kc,
-                                                      T* __restrict__ wt) {
-  const int pc = blockIdx.x * 256 + threadIdx.x;
-  if (pc >= g.M) return;
+__global__ void __launch_bounds__(TN_NODES) taps_nd_kernel(Geom g, WinPoly<T> wp, const T* __restrict__ kc,
+                                                           T* __restrict__ wt, int* __restrict__ cl) {
+  constexpr int ROW = D * 2 * M, RS = ROW + 1;
+  __shared__ T s[TN_NODES * RS];
+  const long long p0 = (long long)blockIdx.x * TN_NODES;
+  const long long pc = p0 + threadIdx.x;
+  if (pc < g.M) {
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    double frac;
-    node_cell((double)kc[(long long)d * g.M + pc], g.Ntd[d], g.Nt[d], frac);
-    T w[2 * M];
-    window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w);
+    for (int d = 0; d < D; ++d) {
+      double frac;
+      const int c = node_cell((double)kc[(long long)d * g.M + pc], g.Ntd[d], g.Nt[d], frac);
+      if (cl != nullptr && d == D - 1) cl[pc] = c;  // last-dimension cell (warp-block adjoint)
+      T w[2 * M];
+      window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w);
 #pragma unroll
-    for (int t = 0; t < 2 * M; ++t) wt[((long long)pc * D + d) * 2 * M + t] = w[t];
+      for (int t = 0; t < 2 * M; ++t) s[threadIdx.x * RS + d * 2 * M + t] = w[t];
+    }
+  }
+  __syncthreads();
+  const int n = (int)(g.M - p0 < TN_NODES ? g.M - p0 : TN_NODES);
+  T* out = wt + p0 * ROW;
+  for (int i = threadIdx.x; i < n * ROW; i += TN_NODES) {
+    const int node = i / ROW, k = i - node * ROW;
+    out[i] = s[node * RS + k];
   }
 }
 
