@@ -51,7 +51,7 @@ struct WbCfg {
   static constexpr int SLOT = (TAPB + 2 * (int)sizeof(T) + 4 + 15) & ~15;
   static constexpr int TCP = TAPB % 16 == 0 ? 16 : (TAPB % 8 == 0 ? 8 : 4);  // cp.async granularity of the taps
   static constexpr size_t BUF = (size_t)WB_NB * SLOT;
-  static constexpr size_t WARP_BYTES = (2 * BUF + 2 * WB_NB * 4 + (size_t)(2 * NE + 2) * 4 + 15) & ~(size_t)15;
+  static constexpr size_t WARP_BYTES = (2 * BUF + 2 * WB_NB * 8 + (size_t)(2 * NE + 2) * 4 + 15) & ~(size_t)15;
 };
 
 template <int BYTES>
@@ -86,9 +86,8 @@ __global__ void __launch_bounds__(256) permute_f_kernel(const typename cplx<T>::
 // block gets tap k0 - U0 + 2m - 1 of dimension 0, so only the k0 in reach of the
 // plane are accumulated.
 template <typename T, int D, int M, int U0>
-__device__ __forceinline__ void wb_visit(int nn, const unsigned char* __restrict__ buf, const int* __restrict__ su1,
-                                         int a_last, int NtL, int ly1, int lyl,
-                                         typename cplx<T>::type (&acc)[WB_K0]) {
+__device__ __forceinline__ void wb_visit(int nn, const unsigned char* __restrict__ buf, const int2* __restrict__ su,
+                                         int ly1, int lyl, typename cplx<T>::type (&acc)[WB_K0]) {
   using C = typename cplx<T>::type;
   using Cfg = WbCfg<T, D, M>;
   constexpr int TAPS = 2 * M;
@@ -98,16 +97,14 @@ __device__ __forceinline__ void wb_visit(int nn, const unsigned char* __restrict
   for (int n = 0; n < nn; ++n) {
     const unsigned char* sl = buf + n * Cfg::SLOT;
     const T* w = reinterpret_cast<const T*>(sl);
-    const C v = *reinterpret_cast<const C*>(sl + Cfg::TAPB);
-    int ul = *reinterpret_cast<const int*>(sl + Cfg::TAPB + 2 * sizeof(T)) - a_last;  // window-local last cell
-    if (ul < 0) ul += NtL;
-    else if (ul >= NtL) ul -= NtL;
-    const int ll = lyl - ul + TAPS - 1;
+    const int2 u = su[n];  // (u1 - 2m + 1, wrap correction - a_last - 2m + 1)
+    const int ll = lyl - (*reinterpret_cast<const int*>(sl + Cfg::TAPB + 2 * sizeof(T)) + u.y);  // last-dim tap
     T c = (unsigned)ll < (unsigned)TAPS ? w[(D - 1) * TAPS + ll] : (T)0;
     if (D == 3) {
-      const int l1 = ly1 - su1[n] + TAPS - 1;
+      const int l1 = ly1 - u.x;
       c *= (unsigned)l1 < (unsigned)TAPS ? w[TAPS + l1] : (T)0;
     }
+    const C v = *reinterpret_cast<const C*>(sl + Cfg::TAPB);
     const T cx = c * v.x, cy = c * v.y;
 #pragma unroll
     for (int k = KLO; k <= KHI; ++k) {
@@ -119,11 +116,11 @@ __device__ __forceinline__ void wb_visit(int nn, const unsigned char* __restrict
 }
 
 template <typename T, int D, int M, int U0 = 0>
-__device__ __forceinline__ void wb_visit_plane(int u0, int nn, const unsigned char* buf, const int* su1, int a_last,
-                                               int NtL, int ly1, int lyl, typename cplx<T>::type (&acc)[WB_K0]) {
+__device__ __forceinline__ void wb_visit_plane(int u0, int nn, const unsigned char* buf, const int2* su, int ly1,
+                                               int lyl, typename cplx<T>::type (&acc)[WB_K0]) {
   if constexpr (U0 < WbCfg<T, D, M>::W0) {
-    if (u0 == U0) wb_visit<T, D, M, U0>(nn, buf, su1, a_last, NtL, ly1, lyl, acc);
-    else wb_visit_plane<T, D, M, U0 + 1>(u0, nn, buf, su1, a_last, NtL, ly1, lyl, acc);
+    if (u0 == U0) wb_visit<T, D, M, U0>(nn, buf, su, ly1, lyl, acc);
+    else wb_visit_plane<T, D, M, U0 + 1>(u0, nn, buf, su, ly1, lyl, acc);
   }
 }
 
@@ -152,8 +149,8 @@ __global__ void __launch_bounds__(32 * WB_WARPS) spread_wb_kernel(Geom g, const 
   // ---- shared layout of this warp
   unsigned char* base = smem_raw + (size_t)warp * Cfg::WARP_BYTES;
   unsigned char* sbuf = base;                              // [2][NB] slots
-  int* su1 = reinterpret_cast<int*>(base + 2 * Cfg::BUF);  // [2][NB] window-local dimension-1 row
-  int* epos = su1 + 2 * NB;                                // [NE]     first cell-sorted position of a segment
+  int2* su = reinterpret_cast<int2*>(base + 2 * Cfg::BUF);  // [2][NB] per node: dimension-1 row, last-dim offset
+  int* epos = reinterpret_cast<int*>(su + 2 * NB);          // [NE]     first cell-sorted position of a segment
   int* epre = epos + NE;                                   // [NE + 1] prefix of the segment lengths
   // ---- window segments: row r = (u0, u1), last-dimension cells [YL - m, YL + LL + m - 2]
   const int a_last = YL - M, b_last = YL + Cfg::LL + M - 2;
@@ -217,7 +214,11 @@ __global__ void __launch_bounds__(32 * WB_WARPS) spread_wb_kernel(Geom g, const 
       for (int o = 0; o < Cfg::TAPB; o += Cfg::TCP) wb_cp_async<Cfg::TCP>(sl + o, src + o);
       wb_cp_async<2 * sizeof(T)>(sl + Cfg::TAPB, fc + pos);
       wb_cp_async<4>(sl + Cfg::TAPB + 2 * sizeof(T), cl + pos);
-      su1[slot * NB + lane] = (lo >> 1) - u0 * Cfg::W1;
+      // window-local last cell ul = cl + corr - a_last (corr undoes the wrap of segment A / B), stored
+      // so that a visit forms its tap as lane - (cl + .y) and lane - .x
+      const int seg = lo & 1;
+      const int corr = a_last < 0 ? (seg == 0 ? -NtL : 0) : (b_last >= NtL && seg == 1 ? NtL : 0);
+      su[slot * NB + lane] = make_int2((lo >> 1) - u0 * Cfg::W1 - (TAPS - 1), corr - a_last - (TAPS - 1));
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -248,8 +249,8 @@ __global__ void __launch_bounds__(32 * WB_WARPS) spread_wb_kernel(Geom g, const 
     else asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncwarp();
-    wb_visit_plane<T, D, M>(u0, min(NB, plane_end(u0) - q0), sbuf + (size_t)slot * Cfg::BUF, su1 + slot * NB,
-                            a_last, NtL, ly1, lyl, acc);
+    wb_visit_plane<T, D, M>(u0, min(NB, plane_end(u0) - q0), sbuf + (size_t)slot * Cfg::BUF, su + slot * NB, ly1,
+                            lyl, acc);
     __syncwarp();
     u0 = nu;
     q0 = nq;

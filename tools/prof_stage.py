@@ -1,6 +1,6 @@
 """Run one stage of several configs a few times (target for a single ncu capture).
 
-    python tools/prof_stage.py adj_spread cfg4_3d_64:4 cfg3_2d_512:4 cfg5_radial_s2:4
+    python tools/prof_stage.py adj_spread[,fwd_interp] cfg4_3d_64:4 cfg3_2d_512:4 cfg5_radial_s2:4
 
 Each config: plan + precompute, then REPS launches of the stage on the plan
 stream (no graph, so ncu sees every launch).
@@ -18,7 +18,7 @@ REPS = int(os.environ.get("PROF_REPS", "2"))
 
 
 def main():
-    stage = sys.argv[1]
+    stages = sys.argv[1].split(",")
     dev = torch.device("cuda", 0)
     for spec in sys.argv[2:]:
         cfg, m = spec.split(":")
@@ -32,13 +32,14 @@ def main():
                              stream=st.cuda_stream, check_nodes=False)
             p.run_stage("precompute")
             fo = torch.empty((w["batch"], w["M"]), dtype=p.tdtype_c, device=dev)
-            for _ in range(REPS):
-                if stage == "fwd_interp":
-                    p.run_stage("fwd_deconv", fhat)
-                    p.run_stage("fwd_fft")
-                    p.run_stage("fwd_interp", None, fo)
-                else:
-                    p.run_stage(stage, f)
+            for stage in stages:
+                for _ in range(REPS):
+                    if stage == "fwd_interp":
+                        p.run_stage("fwd_deconv", fhat)
+                        p.run_stage("fwd_fft")
+                        p.run_stage("fwd_interp", None, fo)
+                    else:
+                        p.run_stage(stage, f)
         st.synchronize()
         print(spec, p.info().get("tile"), flush=True)
         p.close()

@@ -1,5 +1,13 @@
-mkdir -p gpurun_out/r01u
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/r01u/pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/r01u/pytest_gpu.log
-for c in cfg2_1d_2e18 cfg3_2d_512 cfg4_3d_64 cfg5_radial_s2 cfg5_radial_s125; do
-  timeout 300 python tools/stage_bench.py $c 4 auto >> gpurun_out/r01u/stage.log 2>&1
-done
+#!/bin/bash
+# ncu --set full of spread_wb (3D, 2D) and interp_cell (3D)
+out=gpurun_out/r01u; mkdir -p $out
+timeout 300 python tools/prof_stage.py adj_spread,fwd_interp cfg4_3d_64:4 cfg3_2d_512:4 > $out/plain.log 2>&1; rc=$?
+echo "plain exit $rc" >> $out/plain.log
+if [ $rc -eq 0 ]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spread_wb|interp_cell" -c 6 \
+     -o $out/full python tools/prof_stage.py adj_spread,fwd_interp cfg4_3d_64:4 cfg3_2d_512:4 > $out/ncu.log 2>&1
+  ncu -i $out/full.ncu-rep --page raw --csv > $out/full_raw.csv 2>/dev/null
+  ncu -i $out/full.ncu-rep --page source --csv --print-source sass > $out/src.csv 2>/dev/null
+fi
+rm -f $out/full.ncu-rep
+ls -la $out

@@ -1,9 +1,9 @@
-mkdir -p gpurun_out/r01v
-python tools/stage_bench.py cfg2_1d_2e18 4 auto > gpurun_out/r01v/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"1c_kernel|cl_place|cl_scan" -s 8 -c 4 \
-    -o gpurun_out/r01v/full python tools/stage_bench.py cfg2_1d_2e18 4 auto > gpurun_out/r01v/ncu.log 2>&1
-ncu -i gpurun_out/r01v/full.ncu-rep --page details > gpurun_out/r01v/details.txt 2>/dev/null
-ncu -i gpurun_out/r01v/full.ncu-rep --page raw --csv > gpurun_out/r01v/raw.csv 2>/dev/null
-for k in cl_place cl_scan interp1c spread1c; do
-ncu -i gpurun_out/r01v/full.ncu-rep --page source --csv -k regex:$k --print-source sass > gpurun_out/r01v/src_$k.csv 2>/dev/null
+#!/bin/bash
+# wblock spread: gpu tests + stage times (2D, 3D) with and without the warp-block path
+out=gpurun_out/r01v; mkdir -p $out
+timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $out/pytest_gpu.log
+for cfg in cfg3_2d_512 cfg4_3d_64; do
+  STAGE_REPS=20 timeout 300 python tools/stage_bench.py $cfg 4 auto >> $out/stages.log 2>&1
+  NFFTB_NO_WB=1 STAGE_REPS=20 timeout 300 python tools/stage_bench.py $cfg 4 auto >> $out/stages_nowb.log 2>&1
 done
+ls -la $out
