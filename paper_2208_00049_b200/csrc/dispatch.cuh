@@ -31,7 +31,7 @@ struct KernelSet {
   void (*interp_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
   void (*spread_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
   // D = 2 batches: row-segment spread, lanes = batch vectors (resample_rowbatch.cuh)
-  void (*spread_rowbatch)(Geom, const C*, int, const T*, const T*, const int*, const int*, C*);
+  void (*spread_rowbatch)(Geom, const C*, int, const T*, const int*, C*);
   void (*taps_nd)(Geom, WinPoly<T>, const T*, T*, int*);
   // D = 2, 3: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
   void (*spread_wb)(Geom, const C*, const int*, const T*, const int*, C*);

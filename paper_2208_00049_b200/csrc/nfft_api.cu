@@ -103,6 +103,7 @@ struct nfft_plan_s {
   bool wbmode = false;       // D = 2, 3 cell mode: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
   size_t wb_bytes = 0;
   void* d_fc = nullptr;      // B * M complex: node values in cell order (warp-block adjoint)
+  int* d_inv = nullptr;      // M: cell-sorted position of every node (batch adjoint)
   int* d_cl = nullptr;       // M: last-dimension cell of every cell-sorted position
 
   void* d_wt = nullptr;      // M * 2m reals: taps of every cell-sorted position
@@ -188,7 +189,7 @@ void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_stage_nodes2, p->d_stage_grid2, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
-                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT, p->d_fc, p->d_cl};
+                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT, p->d_fc, p->d_cl, p->d_inv};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -578,6 +579,11 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
                                                                  (R*)p->d_wt, p->wbmode ? p->d_cl : nullptr);
       ++p->launches;
       CKL();
+      if (p->batchmode) {
+        invert_perm_kernel<<<(unsigned)((p->M + 255) / 256), 256, 0, st>>>(p->d_jc, (int)p->M, p->d_inv);
+        ++p->launches;
+        CKL();
+      }
     }
     if (p->tensor) {  // TENSOR strategy: the 2m taps of every node, in cell order
       const KernelSet<R>& ks = kernels_of<R>(p);
@@ -669,10 +675,10 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     rec(p, 1, 1);
     const unsigned nch = (unsigned)(p->bp / RB_LANES);
     transpose_bm_kernel<T><<<dim3((unsigned)((p->M + 31) / 32), nch), 256, 0, st>>>(f, (int)p->B, (int)p->M, p->bp,
-                                                                                   (C*)p->d_fT);
+                                                                                   p->d_inv, (C*)p->d_fT);
     const unsigned segs = (unsigned)(p->Nt[0] * ((p->Nt[1] + RB_SEG - 1) / RB_SEG));
-    ks.spread_rowbatch<<<dim3(segs, nch), RB_THREADS, p->rb_bytes, st>>>(
-        p->geom, (const C*)p->d_fT, p->bp, (const T*)p->d_kc, (const T*)p->d_wt, p->d_jc, p->d_cstart, grid);
+    ks.spread_rowbatch<<<dim3(segs, nch), RB_THREADS, p->rb_bytes, st>>>(p->geom, (const C*)p->d_fT, p->bp,
+                                                                         (const T*)p->d_wt, p->d_cstart, grid);
     p->launches += 2;
     CKL();
     return NFFT_SUCCESS;
@@ -1128,7 +1134,8 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
                  Nt[1] >= RB_SEG + 2 * m - 1 && !getenv("NFFTB_NO_BATCH_KERNELS");
   p->bp = (int)((p->B + 31) / 32 * 32);
   if (ok && p->batchmode)
-    ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && alloc(&p->d_wt, (size_t)M * D * 2 * m * rs);
+    ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && alloc(&p->d_wt, (size_t)M * D * 2 * m * rs) &&
+         alloc((void**)&p->d_inv, (size_t)M * 4);
   // D = 2, 3 (not batched): warp-block adjoint over the TENSOR taps; the last-dimension window
   // (32 or 8 lanes + 2m - 1 cells) must not wrap onto itself
   p->wbmode = p->cellmode && !p->batchmode && D >= 2 && Nt[D - 1] >= (D == 3 ? 8 : 32) + 2 * m - 1 &&

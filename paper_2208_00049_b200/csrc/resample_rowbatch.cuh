@@ -11,13 +11,15 @@
 // row and one 32-vector chunk (owner-computes: every cell written exactly once,
 // no atomics, no zero pass; the paper's locked merge, becomes
 // reading the halo NODES). Its nodes are those of the 2m window rows in reach,
-// columns [c0 - m, c0 + SEG + m - 2] (contiguous cell-sorted ranges, two when a
-// row wraps). The fine decomposition keeps the dense centre of a radial
+// columns [c0 - m, c0 + SEG + m - 2], walked CELL BY CELL (per-cell ranges of
+// the cell sort): the window column fixes, at compile time, which of the SEG
+// cells a node reaches and with which last-dimension tap, so every multiply-add
+// is a useful one. The fine decomposition keeps the dense centre of a radial
 // trajectory spread over many CTAs (a coarse tile there holds ~5% of all
-// nodes). Each warp accumulates its nodes into private registers (SEG cells x
-// its lane's vector) through zero-padded last-dimension taps (no per-cell
-// predicate); the 8 warps' partial rows are summed in shared memory.
-// Node values travel transposed, f^T[j][b] (one 256-byte row per node, C64),
+// nodes). Each warp accumulates its window rows into private registers (SEG
+// cells x its lane's vector); the 8 warps' partial rows are summed in shared
+// memory. Node values travel transposed AND in cell order, f^T[pos][b] (one
+// 256-byte row per position, C64; consecutive visits read consecutive rows),
 // and the taps of every node are stored by nfft_precompute (taps_nd_kernel,
 // the paper's TENSOR layout): a node is visited by ~11 row segments, so
 // evaluating its taps once saves the per-visit polynomial work.
@@ -30,12 +32,14 @@ namespace nfftb {
 constexpr int RB_THREADS = 256;  // 8 warps
 constexpr int RB_LANES = 32;     // vectors per chunk
 constexpr int RB_SEG = 16;       // cells per CTA (last dimension)
-constexpr int RB_U = 2;          // nodes per warp step (loads in flight together)
 
 // (B, M) -> (M, BP) and back; BP = batch padded to a multiple of 32 (pad rows unused)
+// out[inv[j]][b] = in[b][j]: node values transposed into CELL order (inv = inverse of the
+// cell-sort permutation jc), one 32-vector row per position
 template <typename T>
 __global__ void __launch_bounds__(256) transpose_bm_kernel(const typename cplx<T>::type* __restrict__ in, int B, int M,
-                                                           int BP, typename cplx<T>::type* __restrict__ out) {
+                                                           int BP, const int* __restrict__ inv,
+                                                           typename cplx<T>::type* __restrict__ out) {
   using C = typename cplx<T>::type;
   __shared__ C t[32][33];
   const int j0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
@@ -47,8 +51,14 @@ __global__ void __launch_bounds__(256) transpose_bm_kernel(const typename cplx<T
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
     const int j = j0 + r, b = b0 + tx;
-    if (j < M && b < B) out[(long long)j * BP + b] = t[tx][r];
+    if (j < M && b < B) out[(long long)__ldg(inv + j) * BP + b] = t[tx][r];
   }
+}
+
+// inv[jc[pos]] = pos (precompute, batch adjoint)
+static __global__ void __launch_bounds__(256) invert_perm_kernel(const int* __restrict__ jc, int M, int* __restrict__ inv) {
+  const int pos = blockIdx.x * 256 + threadIdx.x;
+  if (pos < M) inv[jc[pos]] = pos;
 }
 
 template <typename T>
@@ -69,15 +79,9 @@ __global__ void __launch_bounds__(256) transpose_mb_kernel(const typename cplx<T
   }
 }
 
-__host__ __device__ inline int rb_tpad(int M) { return 2 * M + 2 * (RB_SEG - 1); }
-
 __host__ __device__ inline size_t rb_smem_bytes(int M, int rsize) {
-  const size_t csize = 2 * (size_t)rsize;
-  size_t b = (size_t)(RB_THREADS / 32) * RB_U * rb_tpad(M) * rsize;  // per-warp zero-padded taps, RB_U nodes
-  b = (b + 15) & ~(size_t)15;
-  b += (size_t)(RB_THREADS / 32) * RB_SEG * RB_LANES * csize;  // per-warp partial rows
-  b += (size_t)(2 * M * 4 + 4) * 4;                            // window rows: base, posA, lenA, posB
-  return (b + 15) & ~(size_t)15;
+  (void)M;
+  return (size_t)(RB_THREADS / 32) * RB_SEG * RB_LANES * 2 * rsize;  // per-warp partial rows
 }
 
 // Taps of every cell-sorted node, wt[pos][d][t] (the paper's TENSOR layout,
@@ -115,18 +119,72 @@ __global__ void __launch_bounds__(TN_NODES) taps_nd_kernel(Geom g, WinPoly<T> wp
   }
 }
 
-template <typename T, int M>
-__global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 3 : 2) spread_rowbatch_kernel(Geom g, const typename cplx<T>::type* __restrict__ fT,
-                                                                     int BP, const T* __restrict__ kc,
-                                                                     const T* __restrict__ wt,
-                                                                     const int* __restrict__ jc,
-                                                                     const int* __restrict__ cstart,
-                                                                     typename cplx<T>::type* __restrict__ grid) {
+// Visits of the nodes [lo, hi) of window column U (compile-time) of one window
+// row: cell k of the segment gets tap k - U + 2m - 1 of the last dimension, so
+// only the cells in the node's reach are accumulated (no zero products).
+template <typename T, int M, int U>
+__device__ __forceinline__ void rb_visit(int lo, int hi, int lead, const typename cplx<T>::type* __restrict__ fTc,
+                                         int BP, const T* __restrict__ wt, typename cplx<T>::type (&acc)[RB_SEG]) {
   using C = typename cplx<T>::type;
   constexpr int TAPS = 2 * M;
-  constexpr int TPAD = 2 * M + 2 * (RB_SEG - 1);
+  constexpr int KLO = U - TAPS + 1 > 0 ? U - TAPS + 1 : 0;
+  constexpr int KHI = U < RB_SEG - 1 ? U : RB_SEG - 1;
+  constexpr bool VEC = (TAPS * sizeof(T)) % 16 == 0;  // taps rows 16-byte aligned: vector loads
+#pragma unroll 2
+  for (int pos = lo; pos < hi; ++pos) {
+    const C v = fTc[(long long)pos * BP];
+    const T* wp = wt + (long long)pos * 2 * TAPS;
+    const T w0 = __ldg(wp + lead);
+    T w1[TAPS];
+    if constexpr (VEC && sizeof(T) == 4) {
+#pragma unroll
+      for (int t = 0; t < TAPS; t += 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(wp + TAPS + t));
+        w1[t] = q.x; w1[t + 1] = q.y; w1[t + 2] = q.z; w1[t + 3] = q.w;
+      }
+    } else if constexpr (VEC) {
+#pragma unroll
+      for (int t = 0; t < TAPS; t += 2) {
+        const double2 q = __ldg(reinterpret_cast<const double2*>(wp + TAPS + t));
+        w1[t] = q.x; w1[t + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < TAPS; ++t) w1[t] = __ldg(wp + TAPS + t);
+    }
+    const T vx = w0 * v.x, vy = w0 * v.y;
+#pragma unroll
+    for (int k = KLO; k <= KHI; ++k) {
+      const T w = w1[k - U + TAPS - 1];
+      acc[k].x = fma(w, vx, acc[k].x);
+      acc[k].y = fma(w, vy, acc[k].y);
+    }
+  }
+}
+
+template <typename T, int M, int U = 0>
+__device__ __forceinline__ void rb_row(int lo_l, int hi_l, int lead, const typename cplx<T>::type* fTc, int BP,
+                                       const T* wt, typename cplx<T>::type (&acc)[RB_SEG]) {
+  if constexpr (U < RB_SEG + 2 * M - 1) {
+    const int lo = __shfl_sync(0xffffffffu, lo_l, U), hi = __shfl_sync(0xffffffffu, hi_l, U);
+    if (lo < hi) rb_visit<T, M, U>(lo, hi, lead, fTc, BP, wt, acc);
+    rb_row<T, M, U + 1>(lo_l, hi_l, lead, fTc, BP, wt, acc);
+  }
+}
+
+// One CTA owns SEG cells of one grid row for 32 vectors; warp w walks window rows
+// w, w + 8, ... (lead tap 2m - 1 - r), each window column's nodes in cell order
+// (per-cell ranges from cstart, lane u holds column u's), then the warps'
+// partial rows are summed in shared memory and stored coalesced.
+template <typename T, int M>
+__global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_rowbatch_kernel(
+    Geom g, const typename cplx<T>::type* __restrict__ fTc, int BP, const T* __restrict__ wt,
+    const int* __restrict__ cstart, typename cplx<T>::type* __restrict__ grid) {
+  using C = typename cplx<T>::type;
+  constexpr int TAPS = 2 * M;
   constexpr int NW = RB_THREADS / 32;
-  constexpr int WROWS = 2 * M;
+  constexpr int WC = RB_SEG + TAPS - 1;  // window columns
+  static_assert(WC <= 32, "window columns per lane");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b0 = blockIdx.y * RB_LANES;
@@ -134,103 +192,23 @@ __global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 3 : 2) spread_row
   const int nseg = (NtL + RB_SEG - 1) / RB_SEG;
   const int y0 = blockIdx.x / nseg, c0 = (blockIdx.x - y0 * nseg) * RB_SEG;  // binning row, first column
   const int qs = min(RB_SEG, NtL - c0);
-  T* ptap = reinterpret_cast<T*>(smem_raw) + warp * RB_U * TPAD;  // this warp's padded taps [RB_U][TPAD]
-  C* part = reinterpret_cast<C*>(smem_raw + ((NW * RB_U * TPAD * sizeof(T) + 15) & ~(size_t)15));  // [NW][SEG][32]
-  int* rbase = reinterpret_cast<int*>(part + (size_t)NW * RB_SEG * RB_LANES);             // [WROWS + 1]
-  int* rposA = rbase + WROWS + 1;
-  int* rlenA = rposA + WROWS;
-  int* rposB = rlenA + WROWS;
-  // window rows x0 = y0 - m + r, r = 0..2m-1 (lead tap 2m - 1 - r); columns [c0 - m, c0 + qs + m - 2]
-  const int a_last = c0 - M, b_last = c0 + qs + M - 2;
-  if (tid < WROWS) {
-    const int r = tid;
-    const long long rowkey = (long long)pos_mod(y0 - M + r, Nt0) * NtL;
-    int pA, lA, pB = 0, lB = 0;
-    if (a_last < 0) {
-      pA = cstart[rowkey + NtL + a_last];
-      lA = cstart[rowkey + NtL] - pA;
-      pB = cstart[rowkey];
-      lB = cstart[rowkey + b_last + 1] - pB;
-    } else if (b_last >= NtL) {
-      pA = cstart[rowkey + a_last];
-      lA = cstart[rowkey + NtL] - pA;
-      pB = cstart[rowkey];
-      lB = cstart[rowkey + b_last - NtL + 1] - pB;
-    } else {
-      pA = cstart[rowkey + a_last];
-      lA = cstart[rowkey + b_last + 1] - pA;
-    }
-    rposA[r] = pA;
-    rlenA[r] = lA;
-    rposB[r] = pB;
-    rbase[r] = lA + lB;
-  }
-  for (int i = lane; i < RB_U * TPAD; i += 32) ptap[i] = (T)0;  // padding stays zero; taps at SEG - 1 ..
-  __syncthreads();
-  if (tid == 0) {
-    int run = 0;
-    for (int r = 0; r < WROWS; ++r) {
-      const int c = rbase[r];
-      rbase[r] = run;
-      run += c;
-    }
-    rbase[WROWS] = run;
-  }
-  __syncthreads();
-  const int total = rbase[WROWS];
+  C* part = reinterpret_cast<C*>(smem_raw);  // [NW][SEG][32]
   C acc[RB_SEG];
 #pragma unroll
   for (int k = 0; k < RB_SEG; ++k) {
     acc[k].x = (T)0;
     acc[k].y = (T)0;
   }
-  // warp w takes the window's nodes w, w + NW, ... (warp-uniform: lanes = batch vectors), RB_U at a
-  // time: every load of the RB_U nodes is in flight before the multiply-adds
-  for (int s0 = warp; s0 < total; s0 += NW * RB_U) {
-    C v[RB_U];
-    T vr[RB_U], vi[RB_U];
-    int o[RB_U];
-#pragma unroll
-    for (int u = 0; u < RB_U; ++u) {
-      const int s = s0 + u * NW;
-      v[u].x = (T)0;
-      v[u].y = (T)0;
-      vr[u] = (T)0;
-      o[u] = 0;
-      if (s < total) {
-        int r = 0;
-#pragma unroll
-        for (int q = 1; q < WROWS; ++q) r += rbase[q] <= s;
-        const int within = s - rbase[r];
-        const int pos = within < rlenA[r] ? rposA[r] + within : rposB[r] + (within - rlenA[r]);
-        v[u] = fT[(long long)__ldg(jc + pos) * BP + b0 + lane];
-        const T* wp_ = wt + (long long)pos * 2 * TAPS;
-        vr[u] = __ldg(wp_ + (TAPS - 1 - r));  // lead tap for row y0 (scaled below)
-        if (lane < TAPS) ptap[u * TPAD + RB_SEG - 1 + lane] = __ldg(wp_ + TAPS + lane);
-        double frac;
-        int oo = node_cell((double)__ldg(kc + g.M + pos), g.Ntd[1], NtL, frac) - a_last;  // window column
-        if (oo < 0) oo += NtL;
-        else if (oo >= NtL) oo -= NtL;
-        o[u] = oo;
-      } else if (lane < TAPS) {
-        ptap[u * TPAD + RB_SEG - 1 + lane] = (T)0;
-      }
+  fTc += b0 + lane;
+  for (int r = warp; r < TAPS; r += NW) {  // window row x0 = y0 - m + r
+    const long long rowkey = (long long)pos_mod(y0 - M + r, Nt0) * NtL;
+    int lo_l = 0, hi_l = 0;
+    if (lane < WC) {  // window column u = lane: binning column c0 - m + u
+      const int col = pos_mod(c0 - M + lane, NtL);
+      lo_l = __ldg(cstart + rowkey + col);
+      hi_l = __ldg(cstart + rowkey + col + 1);
     }
-    __syncwarp();
-#pragma unroll
-    for (int u = 0; u < RB_U; ++u) {
-      vi[u] = vr[u] * v[u].y;
-      vr[u] = vr[u] * v[u].x;
-      // cell k (window column k + m) gets tap k - o + 2m - 1, padded index + SEG - 1
-      const T* tp = ptap + u * TPAD + (TAPS - 1 + RB_SEG - 1 - o[u]);
-#pragma unroll
-      for (int k = 0; k < RB_SEG; ++k) {
-        const T w = tp[k];
-        acc[k].x = fma(w, vr[u], acc[k].x);
-        acc[k].y = fma(w, vi[u], acc[k].y);
-      }
-    }
-    __syncwarp();
+    rb_row<T, M>(lo_l, hi_l, TAPS - 1 - r, fTc, BP, wt, acc);
   }
   // sum the warps' partial rows, coalesced stores (consecutive threads = consecutive cells of a vector)
 #pragma unroll
