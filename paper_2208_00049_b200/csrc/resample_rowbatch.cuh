@@ -18,7 +18,8 @@
 // trajectory spread over many CTAs (a coarse tile there holds ~5% of all
 // nodes). Each warp accumulates its window rows into private registers (SEG
 // cells x its lane's vector); the 8 warps' partial rows are summed in shared
-// memory. Node values travel transposed AND in cell order, f^T[pos][b] (one
+// memory (dealing the window columns round-robin to the warps instead, for
+// balance, measured slower: every warp then waits on every row's cstart loads). Node values travel transposed AND in cell order, f^T[pos][b] (one
 // 256-byte row per position, C64; consecutive visits read consecutive rows),
 // and the taps of every node are stored by nfft_precompute (taps_nd_kernel,
 // the paper's TENSOR layout): a node is visited by ~11 row segments, so
@@ -32,6 +33,7 @@ namespace nfftb {
 constexpr int RB_THREADS = 256;  // 8 warps
 constexpr int RB_LANES = 32;     // vectors per chunk
 constexpr int RB_SEG = 16;       // cells per CTA (last dimension)
+constexpr int RB_PITCH = 33;     // partial-row pitch in shared memory (vectors + 1)
 
 // (B, M) -> (M, BP) and back; BP = batch padded to a multiple of 32 (pad rows unused)
 // out[inv[j]][b] = in[b][j]: node values transposed into CELL order (inv = inverse of the
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(256) transpose_mb_kernel(const typename cplx<T
 
 __host__ __device__ inline size_t rb_smem_bytes(int M, int rsize) {
   (void)M;
-  return (size_t)(RB_THREADS / 32) * RB_SEG * RB_LANES * 2 * rsize;  // per-warp partial rows
+  return (size_t)(RB_THREADS / 32) * RB_SEG * RB_PITCH * 2 * rsize;  // per-warp partial rows
 }
 
 // Taps of every cell-sorted node, wt[pos][d][t] (the paper's TENSOR layout,
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_row
   const int nseg = (NtL + RB_SEG - 1) / RB_SEG;
   const int y0 = blockIdx.x / nseg, c0 = (blockIdx.x - y0 * nseg) * RB_SEG;  // binning row, first column
   const int qs = min(RB_SEG, NtL - c0);
-  C* part = reinterpret_cast<C*>(smem_raw);  // [NW][SEG][32]
+  C* part = reinterpret_cast<C*>(smem_raw);  // [NW][SEG][RB_PITCH]
   C acc[RB_SEG];
 #pragma unroll
   for (int k = 0; k < RB_SEG; ++k) {
@@ -210,9 +212,10 @@ __global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_row
     }
     rb_row<T, M>(lo_l, hi_l, TAPS - 1 - r, fTc, BP, wt, acc);
   }
-  // sum the warps' partial rows, coalesced stores (consecutive threads = consecutive cells of a vector)
+  // sum the warps' partial rows (row pitch 33 vectors: conflict-free), coalesced stores (consecutive
+  // threads = consecutive cells of a vector)
 #pragma unroll
-  for (int k = 0; k < RB_SEG; ++k) part[((size_t)warp * RB_SEG + k) * RB_LANES + lane] = acc[k];
+  for (int k = 0; k < RB_SEG; ++k) part[((size_t)warp * RB_SEG + k) * RB_PITCH + lane] = acc[k];
   __syncthreads();
   const int nbc = min(RB_LANES, g.B - b0);
   const long long rowoff = (long long)pos_mod(y0 - (Nt0 >> 1), Nt0) * NtL;
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_row
     a.y = (T)0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      const C c = part[((size_t)w * RB_SEG + k) * RB_LANES + bb];
+      const C c = part[((size_t)w * RB_SEG + k) * RB_PITCH + bb];
       a.x += c.x;
       a.y += c.y;
     }

@@ -1,5 +1,9 @@
-mkdir -p gpurun_out/r01y
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/r01y/pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/r01y/pytest_gpu.log
-for c in cfg2_1d_2e18 cfg3_2d_512 cfg4_3d_64 cfg5_radial_s2 cfg5_radial_s125; do
-  timeout 300 python tools/stage_bench.py $c 4 auto >> gpurun_out/r01y/stage.log 2>&1
+#!/bin/bash
+# cell-ordered batch adjoint: gpu tests + radial stage times (batch kernels on / off)
+out=gpurun_out/r01y; mkdir -p $out
+timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $out/pytest_gpu.log
+for cfg in cfg5_radial_s2 cfg5_radial_s125; do
+  STAGE_REPS=5 timeout 300 python tools/stage_bench.py $cfg 4 auto >> $out/stages.log 2>&1
+  NFFTB_NO_BATCH_KERNELS=1 STAGE_REPS=5 timeout 300 python tools/stage_bench.py $cfg 4 auto >> $out/stages_nobatch.log 2>&1
 done
+ls -la $out
