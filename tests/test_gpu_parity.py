@@ -603,3 +603,84 @@ def test_seam_and_out_of_range_nodes(case):
     w = dict(nodes=nodes, N=N, m=3, sigma=2.0, precision="c128", batch=B,
              fhat=workloads.complex_normal(rng, (B,) + N), f=workloads.complex_normal(rng, (B, len(nodes))))
     _check(w)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["2d_m4", "2d_m1_c64", "2d_m8_ragged", "2d_b3", "3d_m4", "3d_m2_ragged_c64",
+                                  "3d_m8", "3d_2m2", "3d_b2_c64"])
+def test_warp_block_adjoint(case):
+    """D = 2, 3 adjoint over warp-owned cell blocks (resample_wblock.cuh): the
+    default when the last dimension holds the block's window. Grids that are
+    not multiples of the block (8 x 32 / 8 x 4 x 8 cells), wrapped windows,
+    m = 1..8, the 2m+2 window, batches, c64 / c128 against the oracle."""
+    kw = {}
+    if case == "2d_m4":
+        w = workloads.make("cfg3_2d_512", seed=21, N=(40, 64), M=3000, m=4)
+    elif case == "2d_m1_c64":
+        w = workloads.make("cfg5_radial_s2", seed=22, N=(24, 40), M=1500, m=1, batch=1)
+    elif case == "2d_m8_ragged":
+        w = workloads.make("cfg3_2d_512", seed=23, N=(26, 42), M=2500, m=8)
+    elif case == "2d_b3":
+        w = workloads.make("cfg3_2d_512", seed=24, N=(30, 48), M=2000, m=4, batch=3)
+    elif case == "3d_m4":
+        w = workloads.make("cfg4_3d_64", seed=25, N=(12, 10, 16), M=3000, m=4)
+    elif case == "3d_m2_ragged_c64":
+        w = workloads.make("cfg4_3d_64", seed=26, N=(10, 6, 14), M=2000, m=2)
+        w = dict(w, precision="c64", nodes=w["nodes"].astype(np.float32), fhat=w["fhat"].astype(np.complex64),
+                 f=w["f"].astype(np.complex64))
+    elif case == "3d_m8":
+        w = workloads.make("cfg4_3d_64", seed=27, N=(16, 16, 12), M=1500, m=8)
+    elif case == "3d_2m2":
+        w = workloads.make("cfg4_3d_64", seed=28, N=(12, 12, 12), M=1500, m=3)
+        kw = {"window_points": "2m+2"}
+    else:
+        w = workloads.make("cfg4_3d_64", seed=29, N=(8, 12, 10), M=1200, m=3, batch=2)
+        w = dict(w, precision="c64", nodes=w["nodes"].astype(np.float32), fhat=w["fhat"].astype(np.complex64),
+                 f=w["f"].astype(np.complex64))
+    plan = _plan(w, **kw)
+    feats = plan.features()
+    plan.close()
+    assert "wblock" in feats, feats
+    if kw:
+        torch = _torch()
+        plan = _plan(w, **kw)
+        got_y = plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
+        plan.close()
+        nodes = w["nodes"].astype(np.float64)
+        for b in range(w["batch"]):
+            ry = onfft.adjoint(nodes, w["f"][b].astype(np.complex128), w["N"], w["m"], w["sigma"],
+                               window_points="2m+2")
+            assert rel_l2(got_y[b], ry) <= TOL[w["precision"]]
+    else:
+        _check(w)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D", [2, 3])
+def test_warp_block_shards_and_fallback(D, monkeypatch):
+    """Node shards through the warp-block adjoint sum to the full adjoint; the
+    spread_cell fallback (NFFTB_NO_WB) agrees with it."""
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    from paper_2208_00049_b200 import dist
+    if D == 2:
+        w = workloads.make("cfg3_2d_512", seed=31, N=(32, 48), M=4000, m=4)
+    else:
+        w = workloads.make("cfg4_3d_64", seed=32, N=(12, 12, 12), M=3000, m=3)
+    _, full_y, _ = _run(w)
+    _, ry = _oracle(w)
+    assert rel_l2(full_y[0], ry[0]) <= TOL["c128"]
+    nodes = torch.from_numpy(w["nodes"]).cuda()
+    acc = np.zeros_like(full_y)
+    for rank in range(3):
+        plan = pkg.NfftPlan(nodes, w["N"], m=w["m"], node_range=dist.shard_range(w["M"], rank, 3)).precompute()
+        assert "wblock" in plan.features()
+        acc += plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
+        plan.close()
+    assert rel_l2(acc, full_y) < 1e-14
+    monkeypatch.setenv("NFFTB_NO_WB", "1")
+    plan = _plan(w)
+    assert "wblock" not in plan.features()
+    y_cell = plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
+    plan.close()
+    assert rel_l2(y_cell, full_y) < 1e-14
