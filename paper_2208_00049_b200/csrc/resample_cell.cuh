@@ -71,30 +71,42 @@ __global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel
   const int Lp = g.L[D - 1];  // region row pitch (cells): >= Q + EXT, multiple of 8 for C128
   const int R1 = D == 3 ? g.L[1] : 1;
   auto stage = [&](const C* src) {
+    // warp w stages region rows w, w + 8, ...; the row's (i0, i1) and its wrapped source rows advance
+    // incrementally (no division / modulo per row)
     const int rows = D == 2 ? Rr[0] : Rr[0] * Rr[1];
     const int NtL = g.Nt[D - 1];
-    for (int r = warp; r < rows; r += RC_THREADS / 32) {
-      long long off;
-      int srow;
-      if (D == 2) {
-        int s = s0[0] + r;
-        while (s >= g.Nt[0]) s -= g.Nt[0];
-        off = (long long)s * NtL;
-        srow = r;
-      } else {
-        const int i0 = r / Rr[1], i1 = r - i0 * Rr[1];
-        int sa = s0[0] + i0, sb = s0[1] + i1;
-        while (sa >= g.Nt[0]) sa -= g.Nt[0];
-        while (sb >= g.Nt[1]) sb -= g.Nt[1];
-        off = ((long long)sa * g.Nt[1] + sb) * NtL;
-        srow = i0 * R1 + i1;
-      }
+    constexpr int NWS = RC_THREADS / 32;
+    int i0 = D == 2 ? warp : warp / Rr[1], i1 = D == 2 ? 0 : warp - (warp / Rr[1]) * Rr[1];
+    int sa = s0[0] + i0, sb = D == 3 ? s0[1] + i1 : 0;
+    while (sa >= g.Nt[0]) sa -= g.Nt[0];
+    if (D == 3)
+      while (sb >= g.Nt[1]) sb -= g.Nt[1];
+    for (int r = warp; r < rows; r += NWS) {
+      const long long off = D == 2 ? (long long)sa * NtL : ((long long)sa * g.Nt[1] + sb) * NtL;
+      const int srow = D == 2 ? i0 : i0 * R1 + i1;
       const C* rsrc = src + off;
       C* rdst = tile + (long long)srow * Lp;
       for (int col = lane; col < Rr[D - 1]; col += 32) {
-        int s = s0[D - 1] + col;
-        while (s >= NtL) s -= NtL;
-        cp_async_cell<T>(rdst + col, rsrc + s);
+        int sc = s0[D - 1] + col;
+        while (sc >= NtL) sc -= NtL;
+        cp_async_cell<T>(rdst + col, rsrc + sc);
+      }
+      // next row: r + NWS
+      if (D == 2) {
+        i0 += NWS;
+        sa += NWS;
+        while (sa >= g.Nt[0]) sa -= g.Nt[0];
+      } else {
+        i1 += NWS;
+        sb += NWS;
+        while (i1 >= Rr[1]) {  // carry into dimension 0
+          i1 -= Rr[1];
+          sb -= Rr[1];
+          ++i0;
+          if (++sa >= g.Nt[0]) sa -= g.Nt[0];
+        }
+        while (sb >= g.Nt[1]) sb -= g.Nt[1];
+        while (sb < 0) sb += g.Nt[1];
       }
     }
   };
