@@ -1,0 +1,5 @@
+#!/bin/bash
+# end-of-session evidence at HEAD: gpu tests, smoke, bench + ncu (tools/gpu_round.sh), per-config bench lines
+bash tools/gpu_round.sh r01g
+bash tools/config_sweep.sh gpurun_out/r01g/sweep
+ls -la gpurun_out/r01g/sweep
