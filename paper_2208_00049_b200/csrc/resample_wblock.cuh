@@ -33,7 +33,7 @@
 
 namespace nfftb {
 
-constexpr int WB_K0 = 8;     // cells along dimension 0 per warp (registers)
+constexpr int WB_K0 = 16;    // cells along dimension 0 per warp (registers)
 constexpr int WB_WARPS = 4;  // independent warps per CTA
 constexpr int WB_NB = 16;    // nodes per staged batch (two batches in flight per warp)
 
