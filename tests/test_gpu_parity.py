@@ -607,7 +607,7 @@ def test_seam_and_out_of_range_nodes(case):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", ["2d_m4", "2d_m1_c64", "2d_m8_ragged", "2d_b3", "3d_m4", "3d_m2_ragged_c64",
-                                  "3d_m8", "3d_2m2", "3d_b2_c64"])
+                                  "3d_m8", "3d_2m2", "3d_b2_c64", "2d_short_dim0", "3d_short_dim0"])
 def test_warp_block_adjoint(case):
     """D = 2, 3 adjoint over warp-owned cell blocks (resample_wblock.cuh): the
     default when the last dimension holds the block's window. Grids that are
@@ -630,6 +630,10 @@ def test_warp_block_adjoint(case):
                  f=w["f"].astype(np.complex64))
     elif case == "3d_m8":
         w = workloads.make("cfg4_3d_64", seed=27, N=(16, 16, 12), M=1500, m=8)
+    elif case == "2d_short_dim0":  # Nt_0 = 12 < the block's 16 dim-0 cells: window planes repeat
+        w = workloads.make("cfg3_2d_512", seed=33, N=(6, 40), M=800, m=2)
+    elif case == "3d_short_dim0":  # Nt = (8, 12, 20)
+        w = workloads.make("cfg4_3d_64", seed=34, N=(4, 6, 10), M=700, m=2)
     elif case == "3d_2m2":
         w = workloads.make("cfg4_3d_64", seed=28, N=(12, 12, 12), M=1500, m=3)
         kw = {"window_points": "2m+2"}
