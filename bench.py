@@ -76,7 +76,8 @@ def algorithmic(w, deg_fp64=True):
     """Per-launch algorithmic bytes and flops:
     resampling: B*c*prod(Ntilde) + B*c*M + r*D*M bytes,
                 2*M*[B*2*sum_{d=1..D}(2m)^d + 2m*D*deg] flops (deg = 2m, the paper's);
-    deconv/pad: B*c*(prod N + prod Ntilde); crop: 2*B*c*prod N."""
+    deconv/pad: 2*B*c*prod N (the zero padding is written once per plan); crop: 2*B*c*prod N
+    (cell mode: the spread rewrites every cell, so no re-zeroing)."""
     c = 16 if w["precision"] == "c128" else 8
     r = 8 if w["precision"] == "c128" else 4
     D, M, B, m = len(w["N"]), w["M"], w["batch"], w["m"]
@@ -84,7 +85,7 @@ def algorithmic(w, deg_fp64=True):
     nn = int(np.prod(w["N"]))
     res_bytes = B * c * nt + B * c * M + r * D * M
     res_flops = 2 * M * (B * 2 * sum((2 * m) ** d for d in range(1, D + 1)) + 2 * m * D * (2 * m))
-    return dict(resample_bytes=res_bytes, resample_flops=res_flops, deconv_bytes=B * c * (nn + nt),
+    return dict(resample_bytes=res_bytes, resample_flops=res_flops, deconv_bytes=2 * B * c * nn,
                 crop_bytes=2 * B * c * nn, zero_bytes=B * c * nt, grid_cells=nt)
 
 
