@@ -89,7 +89,7 @@ typedef enum {
 } nfft_precompute_strategy;
 
 typedef struct {
-  int64_t batch;          /* B >= 1 transforms sharing the nodes (default 1) */
+  int64_t batch;          /* 1 <= B <= 65535 transforms sharing the nodes (default 1; larger: UNSUPPORTED) */
   int64_t tile[3];        /* block size Q_d in grid cells; 0 = default */
   void* stream;           /* cudaStream_t for all work; NULL = legacy default stream */
   int device;             /* CUDA device ordinal; -1 = current device */

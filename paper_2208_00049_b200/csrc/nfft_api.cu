@@ -968,6 +968,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   nfft_default_options(&opt);
   if (opt_in) opt = *opt_in;
   if (opt.batch < 1) return NFFT_ERROR_INVALID_VALUE;
+  if (opt.batch > 65535) return NFFT_ERROR_UNSUPPORTED;  // batch vectors index grid dimension y
   if (opt.method < 0 || opt.method > 7) return NFFT_ERROR_INVALID_VALUE;
   if (opt.precompute < NFFT_PRECOMPUTE_AUTO || opt.precompute > NFFT_PRECOMPUTE_TENSOR) return NFFT_ERROR_INVALID_VALUE;
   if (!(sigma > 1.0) || !std::isfinite(sigma)) return NFFT_ERROR_BAD_GEOMETRY;

@@ -75,5 +75,12 @@ def test_argument_validation_before_any_device_work(libpath):
     Nodd = (ctypes.c_int64 * 1)(15)
     assert create(ctypes.byref(h), 1, Nodd, 2, nodes, 2.0, 2, 0, 1) == 2
     assert create(ctypes.byref(h), 1, N, 2, nodes, 2.0, 2, 5, 1) == 1   # unknown window
+    # batch outside [1, 65535] (nfft_options.batch)
+    opt = pkg.Options()
+    L.nfft_default_options(ctypes.byref(opt))
+    opt.batch = 65536
+    assert L.nfft_plan_create_ex(ctypes.byref(h), 1, N, 2, nodes, 2.0, 2, 0, 1, ctypes.byref(opt)) == 9
+    opt.batch = 0
+    assert L.nfft_plan_create_ex(ctypes.byref(h), 1, N, 2, nodes, 2.0, 2, 0, 1, ctypes.byref(opt)) == 1
     assert L.nfft_forward(None, nodes, nodes) == 1
     assert L.nfft_precompute(None) == 1
