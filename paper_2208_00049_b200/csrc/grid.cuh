@@ -150,4 +150,55 @@ __global__ void __launch_bounds__(THREADS) crop_kernel(Geom g, const typename cp
   }
 }
 
+// Deconvolution + placement (FWD, Alg. 1 lines 1-3) and crop + deconvolution
+// (!FWD, Alg. 2 lines 7-9, cell mode: no re-zeroing) over a FLATTENED index:
+// one thread per two consecutive last-dimension cells of any row (batch x all
+// but the last dimension), 32-bit index arithmetic (the host guarantees
+// B * prod N / 2 < 2^31). Every thread is busy whatever N_{D-1} is (the
+// row-per-CTA kernels above leave 3/4 of a CTA idle at N = 64 and decode
+// their rows with 64-bit divisions).
+template <typename T, bool FWD>
+__global__ void __launch_bounds__(THREADS) correct_flat_kernel(Geom g, const typename cplx<T>::type* __restrict__ in,
+                                                               const T* __restrict__ beta,
+                                                               typename cplx<T>::type* __restrict__ out) {
+  using C = typename cplx<T>::type;
+  const int D = g.D;
+  const int ntl = g.Nt[D - 1], nl = g.N[D - 1];
+  const int hp = (nl + 1) >> 1;  // cell pairs per row
+  const int units = (int)((long long)g.B * (g.ngrid_cells / nl)) * hp;
+  const T* bl = beta + g.beta_off[D - 1];
+  for (int u = blockIdx.x * THREADS + threadIdx.x; u < units; u += gridDim.x * THREADS) {
+    const int row = u / hp;
+    const int x0 = (u - row * hp) * 2;
+    int r = row;
+    T scale = (T)1;
+    long long lin = 0, mul = 1;  // storage row of the oversampled grid (all but the last dimension)
+    for (int d = D - 2; d >= 0; --d) {
+      const int i = r % g.N[d];
+      r /= g.N[d];
+      const int n = i - (g.N[d] >> 1);
+      scale *= beta[g.beta_off[d] + i];
+      lin += (long long)(n < 0 ? n + g.Nt[d] : n) * mul;
+      mul *= g.Nt[d];
+    }
+    const long long gbase = (long long)r * g.grid_cells + lin * ntl;  // r = batch index
+    const long long nbase = (long long)row * nl;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int x = x0 + v;
+      if (x < nl) {
+        const int n = x - (nl >> 1);
+        const int s = n < 0 ? n + ntl : n;
+        const T sc = scale * bl[x];
+        const C a = FWD ? in[nbase + x] : in[gbase + s];
+        C o;
+        o.x = a.x * sc;
+        o.y = a.y * sc;
+        if (FWD) out[gbase + s] = o;
+        else out[nbase + x] = o;
+      }
+    }
+  }
+}
+
 }  // namespace nfftb

@@ -609,9 +609,16 @@ nfft_status stage_deconv(nfft_plan p, const typename cplx<T>::type* fhat, cudaSt
   const Geom& g = p->geom;
   const int nl = g.N[g.D - 1];
   const long long rows = (long long)g.B * (g.ngrid_cells / nl);
-  dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
-  deconv_place_kernel<T><<<grid, THREADS, 0, st>>>(g, fhat, (const T*)p->d_betaT,
-                                                          (typename cplx<T>::type*)p->d_grid_in);
+  const long long units = rows * ((nl + 1) / 2);
+  if (units < (1LL << 31) - THREADS * 4096LL) {  // flattened, two cells per thread
+    const unsigned ctas = (unsigned)std::min<long long>((units + THREADS - 1) / THREADS, (long long)p->sm_count * 16);
+    correct_flat_kernel<T, true><<<ctas, THREADS, 0, st>>>(g, fhat, (const T*)p->d_betaT,
+                                                           (typename cplx<T>::type*)p->d_grid_in);
+  } else {
+    dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
+    deconv_place_kernel<T><<<grid, THREADS, 0, st>>>(g, fhat, (const T*)p->d_betaT,
+                                                     (typename cplx<T>::type*)p->d_grid_in);
+  }
   ++p->launches;
   CKL();
   return NFFT_SUCCESS;
@@ -772,8 +779,15 @@ nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st) 
   if (p->cellmode) {  // the cell-mode spread rewrites every cell: crop only, no re-zeroing
     const int nl = g.N[g.D - 1];
     const long long rows = (long long)g.B * (g.ngrid_cells / nl);
-    dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
-    crop_kernel<T><<<grid, THREADS, 0, st>>>(g, (const typename cplx<T>::type*)p->d_grid_adj, (const T*)p->d_betaT, y);
+    const long long units = rows * ((nl + 1) / 2);
+    if (units < (1LL << 31) - THREADS * 4096LL) {  // flattened, two cells per thread
+      const unsigned ctas = (unsigned)std::min<long long>((units + THREADS - 1) / THREADS, (long long)p->sm_count * 16);
+      correct_flat_kernel<T, false><<<ctas, THREADS, 0, st>>>(g, (const typename cplx<T>::type*)p->d_grid_adj,
+                                                              (const T*)p->d_betaT, y);
+    } else {
+      dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
+      crop_kernel<T><<<grid, THREADS, 0, st>>>(g, (const typename cplx<T>::type*)p->d_grid_adj, (const T*)p->d_betaT, y);
+    }
     ++p->launches;
     CKL();
     return NFFT_SUCCESS;
