@@ -46,14 +46,24 @@ __global__ void __launch_bounds__(256) transpose_bm_kernel(const typename cplx<T
   __shared__ C t[32][33];
   const int j0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int r = ty; r < 32; r += 8) {
+  int dst[4];  // destination positions of this thread's output rows, loaded with the values
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = j0 + ty + 8 * k;
+    dst[k] = j < M ? __ldg(inv + j) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = ty + 8 * k;
     const int b = b0 + r, j = j0 + tx;
     if (b < B && j < M) t[r][tx] = in[(long long)b * M + j];
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = ty + 8 * k;
     const int j = j0 + r, b = b0 + tx;
-    if (j < M && b < B) out[(long long)__ldg(inv + j) * BP + b] = t[tx][r];
+    if (j < M && b < B) out[(long long)dst[k] * BP + b] = t[tx][r];
   }
 }
 
