@@ -695,7 +695,7 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     // once, no zero pass
     rec(p, 1, 1);
     using C = typename cplx<T>::type;
-    permute_f_kernel<T><<<dim3((unsigned)((p->M + 255) / 256), (unsigned)p->B), 256, 0, st>>>(
+    permute_f_kernel<T><<<dim3((unsigned)((p->M + 1023) / 1024), (unsigned)p->B), 256, 0, st>>>(
         f, p->d_jc, (int)p->M, p->node_begin, p->node_end, (C*)p->d_fc);
     long long nblk = (p->Nt[0] + WB_K0 - 1) / WB_K0;
     if (p->D == 3) nblk *= (p->Nt[1] + 3) / 4 * ((p->Nt[2] + 7) / 8);

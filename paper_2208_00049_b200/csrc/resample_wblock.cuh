@@ -72,14 +72,27 @@ __global__ void __launch_bounds__(256) permute_f_kernel(const typename cplx<T>::
                                                         const int* __restrict__ jc, int M, int nb, int ne,
                                                         typename cplx<T>::type* __restrict__ fc) {
   using C = typename cplx<T>::type;
-  const int pos = blockIdx.x * 256 + threadIdx.x;
-  if (pos >= M) return;
+  constexpr int PF = 4;  // positions per thread: the index loads of all four in flight, then the gathers
   const long long b = blockIdx.y;
-  C v;
-  v.x = (T)0;
-  v.y = (T)0;
-  if (pos >= nb && pos < ne) v = f[b * M + __ldg(jc + pos)];
-  fc[b * M + pos] = v;
+  const int p0 = blockIdx.x * 256 * PF + threadIdx.x;
+  int j[PF];
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    const int pos = p0 + k * 256;
+    j[k] = (pos < M && pos >= nb && pos < ne) ? __ldg(jc + pos) : -1;
+  }
+  C v[PF];
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    v[k].x = (T)0;
+    v[k].y = (T)0;
+    if (j[k] >= 0) v[k] = f[b * M + j[k]];
+  }
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    const int pos = p0 + k * 256;
+    if (pos < M) fc[b * M + pos] = v[k];
+  }
 }
 
 // Visits of the nn staged nodes of window plane U0 (compile-time): cell k0 of the
