@@ -65,9 +65,11 @@ typedef enum {
 
 /* Resampling kernels. */
 typedef enum {
-  NFFT_METHOD_AUTO = 0,   /* tiled when the tile+halo fits shared memory */
-  NFFT_METHOD_TILED = 1,  /* Alg. 3/4: grid tile + m-halo staged in shared memory;
-                             adjoint as a per-cell gather over cell-sorted nodes (D <= 2) */
+  NFFT_METHOD_AUTO = 0,   /* = TILED */
+  NFFT_METHOD_TILED = 1,  /* Alg. 3/4 over CELL-sorted nodes: interpolation per tile
+                             with the tile + m-halo staged in shared memory; owner-computes adjoints
+                             (D = 1 warp segments; D = 2, 3 warp-owned cell blocks over stored taps;
+                             2D batches of >= 8: row segments with lanes = vectors) */
   NFFT_METHOD_DIRECT = 2, /* unblocked resampling straight from L2/HBM */
   NFFT_METHOD_TILED_CAS = 3, /* tiled; adjoint accumulates with shared-memory atomics (reference variant) */
   NFFT_METHOD_TILED_LOC = 4, /* tiled; adjoint lanes-own-cells + global reduction flush (D <= 2) */
@@ -80,7 +82,8 @@ typedef enum {
 
 /* Window precomputation strategy (Fig. 4 at PAPER.md:748-765). */
 typedef enum {
-  NFFT_PRECOMPUTE_AUTO = 0,       /* POLYNOMIAL (measured faster on B200 at every config) */
+  NFFT_PRECOMPUTE_AUTO = 0,       /* POLYNOMIAL (measured faster on B200 at every config); the
+                                     D = 2, 3 adjoints store the taps regardless (precompute table) */
   NFFT_PRECOMPUTE_POLYNOMIAL = 1, /* taps evaluated per call from the piecewise polynomial */
   NFFT_PRECOMPUTE_TENSOR = 2      /* the 2m D taps of every node stored by nfft_precompute (PAPER.md:599-604,
                                      "TENSOR": 2m D M reals; trades FP work for memory traffic);
