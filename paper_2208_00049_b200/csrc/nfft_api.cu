@@ -332,6 +332,7 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
   }
   p->grid_direct = p->sm_count * 8;
+  bool sc_ok = true;  // spread_cell fallback configured (D >= 2 cell mode)
   if (p->cellmode) {
     bool ok = false;
     if (p->D == 1 && ks.interp1 && ks.spread1) {
@@ -362,15 +363,20 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
       int cap = fixed < budget ? (int)std::min<size_t>(2048, (budget - fixed) / slot) : 0;
       const size_t sb = spread_cell_smem_bytes(p->D, p->m, (int)p->rsize(), cap, wrows, wcols);
       int occ_i = 0, occ_s = 0;
-      ok = cap >= 32 && nitems <= 512 && nrows <= 1024 && p->region_bytes <= 200 * 1024 &&
-           cudaFuncSetAttribute((const void*)ks.interp_cell, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)p->region_bytes) == cudaSuccess &&
-           cudaFuncSetAttribute((const void*)ks.spread_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) ==
-               cudaSuccess &&
-           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp_cell, RC_THREADS,
-                                                         p->region_bytes) == cudaSuccess &&
-           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread_cell, 256, sb) == cudaSuccess &&
-           occ_i >= 1 && occ_s >= 1;
+      const bool interp_ok = nrows <= 1024 && p->region_bytes <= 200 * 1024 &&
+                             cudaFuncSetAttribute((const void*)ks.interp_cell, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)p->region_bytes) == cudaSuccess &&
+                             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp_cell, RC_THREADS,
+                                                                           p->region_bytes) == cudaSuccess &&
+                             occ_i >= 1;
+      sc_ok = cap >= 32 && nitems <= 512 &&
+              cudaFuncSetAttribute((const void*)ks.spread_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) ==
+                  cudaSuccess &&
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread_cell, 256, sb) == cudaSuccess &&
+              occ_s >= 1;
+      // the spread_cell fallback's limits only matter when neither the warp-block nor the batch adjoint
+      // takes the plan (checked again below, after those are configured)
+      ok = interp_ok && (sc_ok || p->wbmode || p->batchmode);
       p->sc_cap = cap;
       p->sc_bytes = sb;
     }
@@ -405,6 +411,10 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
       cudaGetLastError();
     }
     p->wbmode = ok;
+  }
+  if (p->cellmode && p->D >= 2 && !p->wbmode && !p->batchmode && !sc_ok) {  // no adjoint for this tile in cell mode
+    p->cellmode = false;
+    p->tensor = false;
   }
   p->use_ind = false;
   if (p->D >= 2 && !p->cellmode && p->tiled && ks.interp_nd &&

@@ -688,3 +688,21 @@ def test_warp_block_shards_and_fallback(D, monkeypatch):
     y_cell = plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
     plan.close()
     assert rel_l2(y_cell, full_y) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["2d_tile_64x64", "radial_tile_32x128"])
+def test_large_tiles_keep_cell_mode(case):
+    """Tiles beyond the spread_cell fallback's limits (more than 512 gather items)
+    stay in cell mode when the warp-block or the batch adjoint takes the plan."""
+    if case == "2d_tile_64x64":
+        w = workloads.make("cfg3_2d_512", seed=41, N=(64, 96), M=3000, m=4)
+        tile, feat = (64, 64), "wblock"
+    else:
+        w = workloads.make("cfg5_radial_s2", seed=42, N=(64, 96), M=2000, m=4, batch=8)
+        tile, feat = (32, 128), "batch"
+    plan = _plan(w, tile=tile)
+    feats = plan.features()
+    plan.close()
+    assert "cell_mode" in feats and feat in feats, feats
+    _check(w, tile=tile)
