@@ -13,11 +13,31 @@ constexpr int MAX_Z = 17;   // polynomial coefficients per tap (degree <= 16)
 constexpr int THREADS = 256;
 
 // Window-table degree (DESIGN.md §Window tables): the paper's degree 2m
-// is raised to 14 in fp64 so the table error (~1e-14 of the
-// peak) stays far below the 1e-12 parity bar; fp32 uses max(2m, 8).
+// is raised in fp64 so the table error stays <= 5e-14 of the
+// peak, far below the 1e-12 parity bar (LSQ fit, sigma = 2 / 1.25: degree 14
+// for m <= 5, degree 12 for m >= 6 — 4.5e-14 at m = 6, 1.4e-14 at m = 8;
+// tools/poly_degree.py); fp32 uses max(2m, 8) (m >= 5) and 8.
 __host__ __device__ constexpr int poly_degree(int m, bool fp64) {
-  return fp64 ? (2 * m > 14 ? 2 * m : 14) : (2 * m > 8 ? 2 * m : 8);
+  return fp64 ? (m <= 5 ? 14 : 12) : (2 * m > 8 ? 2 * m : 8);
 }
+
+// Phase timestamps for the timeline harness (tools/micro/trace1d.cu defines
+// NFFTB_PHASE_TRACE before including the kernels); empty in the library.
+#ifdef NFFTB_PHASE_TRACE
+__device__ unsigned long long nfftb_trace[1 << 16];
+#define NFFTB_TRACE(slot)                                                                          \
+  do {                                                                                             \
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 8192) {                               \
+      unsigned long long t_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      nfftb_trace[blockIdx.x * 8 + (slot)] = t_;                                                   \
+    }                                                                                              \
+  } while (0)
+#else
+#define NFFTB_TRACE(slot) \
+  do {                    \
+  } while (0)
+#endif
 
 template <typename T> struct cplx;
 template <> struct cplx<double> { using type = double2; };
@@ -45,6 +65,18 @@ struct Geom {
 // (taps m..2m-1 are their mirrors, see taps()). Passed as a kernel parameter
 // so every coefficient is a constant-bank operand of the FMA.
 template <typename T> struct WinPoly { T mu[MAX_D][MAX_M][MAX_Z]; };
+
+// The same table cut to the kernel's (D, m, degree): what the resampling
+// kernels take as a parameter. Kernel parameters live in the constant bank,
+// so every coefficient is an immediate operand of the FMA, and a small
+// parameter block keeps the launch cheap (measured on B200: an empty
+// 1024-CTA kernel with the full 3.3 KB table costs 5.9 us per stream launch,
+// 3.9 us without).
+template <typename T, int D, int M>
+struct WinPolyN {
+  static constexpr int Z = poly_degree(M, sizeof(T) == 8) + 1;
+  T mu[D][M][Z];
+};
 
 // Cell of a node along one dimension (reading R5/R10):
 // t = Ntilde * k (one IEEE multiply, never contracted), a = floor(t),
@@ -78,8 +110,9 @@ __device__ __forceinline__ int pos_mod(int a, int n) {
 // Tap l (cell a-m+1+l) and tap 2m-1-l are mirror images, w_{2m-1-l}(zeta) =
 // w_l(-zeta) (the window is even), so with p_l = E(zeta^2) + zeta O(zeta^2):
 // w_l = E + zeta O, w_{2m-1-l} = E - zeta O.
-template <typename T, int M, int DEG>
-__device__ __forceinline__ void window_taps(T zeta, const T (&mu)[MAX_M][MAX_Z], T (&w)[2 * M]) {
+template <typename T, int M, int DEG, int ML, int ZL>
+__device__ __forceinline__ void window_taps(T zeta, const T (&mu)[ML][ZL], T (&w)[2 * M]) {
+  static_assert(ML >= M && ZL > DEG, "window table too small");
   const T z2 = zeta * zeta;
 #pragma unroll
   for (int l = 0; l < M; ++l) {

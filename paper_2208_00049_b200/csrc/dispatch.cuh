@@ -11,8 +11,8 @@ struct KernelSet {
   using C = typename cplx<T>::type;
   void (*interp_tiled)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
   void (*spread_tiled)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
-  void (*interp_direct)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, C*);
-  void (*spread_direct)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, C*);
+  const void* interp_direct;  // takes WinPolyN<T, D, m> (launched with launch_k)
+  const void* spread_direct;  // takes WinPolyN<T, D, m> (launched with launch_k)
   void (*spread_loc)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
   int loc_threads;
   void (*spread_own)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
@@ -20,19 +20,19 @@ struct KernelSet {
   void (*spread_sorted)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, C*);
   void (*spread_gather)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
   // D = 1 static-tile kernels (resample1d.cuh)
-  void (*interp1)(Geom, WinPoly<T>, const C*, const T*, const int*, int, int, int, C*);
-  void (*spread1)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
+  const void* interp1;  // takes WinPolyN<T, D, m> (launched with launch_k)
+  const void* spread1;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 1 TENSOR precompute (taps stored by nfft_precompute) and the adjoint over them
-  void (*taps1)(Geom, WinPoly<T>, const T*, T*);
-  void (*spread1t)(Geom, const C*, const T*, const int*, const int*, int, int, int, C*);
+  const void* taps1;  // takes WinPolyN<T, D, m> (launched with launch_k)
+  const void* spread1t;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 2, 3 static-tile interpolation (resample_nd.cuh)
   void (*interp_nd)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
   // D = 2, 3 over cell-sorted nodes (resample_cell.cuh)
-  void (*interp_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
-  void (*spread_cell)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, int, C*);
+  const void* interp_cell;  // takes WinPolyN<T, D, m> (launched with launch_k)
+  const void* spread_cell;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 2 batches: row-segment spread, lanes = batch vectors (resample_rowbatch.cuh)
   void (*spread_rowbatch)(Geom, const C*, int, const T*, const int*, C*);
-  void (*taps_nd)(Geom, WinPoly<T>, const T*, T*, int*);
+  const void* taps_nd;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 2, 3: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
   void (*spread_wb)(Geom, const C*, const int*, const T*, const int*, C*);
   size_t wb_warp_bytes;
@@ -62,30 +62,35 @@ namespace nfftb {
 template <typename T, int D, int M>
 KernelSet<T> make_set() {
   constexpr int DEG = poly_degree(M, sizeof(T) == 8);
-  KernelSet<T> k{interp_tiled_kernel<T, D, M, DEG>, spread_tiled_kernel<T, D, M, DEG>,
-                 interp_direct_kernel<T, D, M, DEG>, spread_direct_kernel<T, D, M, DEG>, nullptr, 0, nullptr, 0,
-                 spread_sorted_kernel<T, D, M, DEG>, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                 nullptr, nullptr, nullptr, nullptr, nullptr, 0};
-  if constexpr (D == 1) {
-    k.interp1 = interp1c_kernel<T, M, DEG>;
-    k.spread1 = spread1c_kernel<T, M, DEG>;
-    k.taps1 = taps1_kernel<T, M, DEG>;
-    k.spread1t = spread1t_kernel<T, M>;
-  } else {
-    k.interp_nd = interp_nd_kernel<T, D, M, DEG>;
-    k.interp_cell = interp_cell_kernel<T, D, M, DEG>;
-    k.spread_cell = spread_cell_kernel<T, D, M, DEG>;
-    if constexpr (D == 2) k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
-    k.taps_nd = taps_nd_kernel<T, D, M, DEG>;
-    k.spread_wb = spread_wb_kernel<T, D, M>;
-    k.wb_warp_bytes = WbCfg<T, D, M>::WARP_BYTES;
-  }
+  KernelSet<T> k{};
+  k.interp_direct = (const void*)interp_direct_kernel<T, D, M, DEG>;
+  k.spread_direct = (const void*)spread_direct_kernel<T, D, M, DEG>;
+#ifdef NFFTB_TILE_VARIANTS
+  // first-generation tile-mode variants (methods TILED_CAS .. TILED_V1): reference builds only
+  k.interp_tiled = interp_tiled_kernel<T, D, M, DEG>;
+  k.spread_tiled = spread_tiled_kernel<T, D, M, DEG>;
+  k.spread_sorted = spread_sorted_kernel<T, D, M, DEG>;
+  if constexpr (D >= 2) k.interp_nd = interp_nd_kernel<T, D, M, DEG>;
   if constexpr (D <= 2) {
     k.spread_loc = spread_loc_kernel<T, D, M, DEG>;
     k.loc_threads = LocCfg<T, D, M>::THR;
     k.spread_own = spread_own_kernel<T, D, M, DEG>;
     k.own_threads = OwnCfg<T, D, M>::THR;
     k.spread_gather = spread_gather_kernel<T, D, M, DEG>;
+  }
+#endif
+  if constexpr (D == 1) {
+    k.interp1 = (const void*)interp1s_kernel<T, M, DEG>;
+    k.spread1 = (const void*)spread1s_kernel<T, M, DEG, false>;
+    k.taps1 = (const void*)taps1_kernel<T, M, DEG>;
+    k.spread1t = (const void*)spread1s_kernel<T, M, DEG, true>;
+  } else {
+    k.interp_cell = (const void*)interp_cell_kernel<T, D, M, DEG>;
+    k.spread_cell = (const void*)spread_cell_kernel<T, D, M, DEG>;
+    if constexpr (D == 2) k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
+    k.taps_nd = (const void*)taps_nd_kernel<T, D, M, DEG>;
+    k.spread_wb = spread_wb_kernel<T, D, M>;
+    k.wb_warp_bytes = WbCfg<T, D, M>::WARP_BYTES;
   }
   return k;
 }

@@ -68,6 +68,7 @@ struct nfft_plan_s {
   Geom geom{};
   WinPoly<double> wp64{};
   WinPoly<float> wp32{};
+  alignas(16) unsigned char wpn[sizeof(WinPoly<double>)] = {};  // the table cut to (D, m, degree): WinPolyN
   KernelSet<double> k64{};
   KernelSet<float> k32{};
   // device buffers
@@ -90,8 +91,8 @@ struct nfft_plan_s {
   bool cellmode = false;
   bool tile_binned = false;  // cell mode: perm/offsets (tile sort) computed on demand for nfft_get_binning
   int64_t ncells = 0;        // prod Ntilde
-  size_t r1_spread_bytes = 0;
-  int s1_occ = 1;            // spread1c CTAs resident per SM
+  size_t r1_spread_bytes = 0; // spread1s shared memory
+  size_t r1_interp_bytes = 0; // interp1s shared memory
   size_t sc_bytes = 0;       // spread_cell shared memory
   int sc_cap = 0;            // spread_cell node slots per chunk
   void* d_kc = nullptr;      // D*M reals: coordinates in cell order (SoA)
@@ -208,6 +209,23 @@ inline void rec(nfft_plan p, int which, int slot) {
   if (p->events) cudaEventRecord(p->ev[which][slot], p->stream);
 }
 
+// Launches a kernel taken by pointer (KernelSet members typed const void*); the
+// arguments are passed by address, the window table as the plan's packed
+// WinPolyN bytes (the runtime copies the kernel's parameter size from it).
+struct WpnArg {
+  const unsigned char* bytes;
+};
+template <typename A>
+inline void* arg_ptr(A& a) {
+  return (void*)&a;
+}
+inline void* arg_ptr(WpnArg& a) { return (void*)a.bytes; }
+template <typename... A>
+cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... a) {
+  void* args[] = {arg_ptr(a)...};
+  return cudaLaunchKernel(fn, grid, block, args, smem, st);
+}
+
 template <typename T>
 nfft_status build_window_tables(nfft_plan p) {
   const int n = (int)(p->N[0] + (p->D > 1 ? p->N[1] : 0) + (p->D > 2 ? p->N[2] : 0));
@@ -240,6 +258,15 @@ nfft_status build_window_tables(nfft_plan p) {
         p->wp32.mu[d][l][z] = (float)v;
       }
   delete[] host;
+  // packed [d][l][z] table for the kernels' WinPolyN<T, D, m> parameter (z <= degree)
+  const int Z = p->deg + 1;
+  for (int d = 0; d < p->D; ++d)
+    for (int l = 0; l < p->m; ++l)
+      for (int z = 0; z < Z; ++z) {
+        const size_t i = ((size_t)d * p->m + l) * Z + z;
+        if (sizeof(T) == 8) reinterpret_cast<double*>(p->wpn)[i] = p->wp64.mu[d][l][z];
+        else reinterpret_cast<float*>(p->wpn)[i] = p->wp32.mu[d][l][z];
+      }
   return NFFT_SUCCESS;
 }
 
@@ -336,15 +363,21 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
   if (p->cellmode) {
     bool ok = false;
     if (p->D == 1 && ks.interp1 && ks.spread1) {
-      const size_t sb = (size_t)S1_WARPS * s1_warp_bytes(p->m, p->csize(), p->rsize());
-      int occ_s = 0;
+      const size_t sb = s1_smem_bytes(p->m, p->csize(), p->rsize());
+      const size_t ib = i1_smem_bytes(p->m, p->csize());
+      int occ_s = 0, occ_t = 0, occ_i = 0;
       ok = cudaFuncSetAttribute((const void*)ks.spread1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) ==
                cudaSuccess &&
-           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, 32 * S1_WARPS, sb) ==
+           cudaFuncSetAttribute((const void*)ks.spread1t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb) ==
                cudaSuccess &&
-           occ_s >= 1;
+           cudaFuncSetAttribute((const void*)ks.interp1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib) ==
+               cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, S1_THREADS, sb) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, (const void*)ks.spread1t, S1_THREADS, sb) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp1, I1_THREADS, ib) == cudaSuccess &&
+           occ_s >= 1 && occ_t >= 1 && occ_i >= 1;
       p->r1_spread_bytes = sb;
-      p->s1_occ = occ_s;
+      p->r1_interp_bytes = ib;
     }
     if (p->D >= 2 && ks.interp_cell && ks.spread_cell) {
       int wrows = 1;
@@ -585,10 +618,9 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
     p->tile_binned = false;
     if (p->batchmode || p->wbmode) {  // taps of every node for the D >= 2 adjoint (TENSOR layout)
       const KernelSet<R>& ks = kernels_of<R>(p);
-      ks.taps_nd<<<(unsigned)((p->M + TN_NODES - 1) / TN_NODES), TN_NODES, 0, st>>>(p->geom, poly_of<R>(p), (const R*)p->d_kc,
-                                                                 (R*)p->d_wt, p->wbmode ? p->d_cl : nullptr);
+      CK(launch_k(ks.taps_nd, (unsigned)((p->M + TN_NODES - 1) / TN_NODES), TN_NODES, 0, st, p->geom, WpnArg{p->wpn},
+                  (const R*)p->d_kc, (R*)p->d_wt, p->wbmode ? p->d_cl : (int*)nullptr));
       ++p->launches;
-      CKL();
       if (p->batchmode) {
         invert_perm_kernel<<<(unsigned)((p->M + 255) / 256), 256, 0, st>>>(p->d_jc, (int)p->M, p->d_inv);
         ++p->launches;
@@ -597,11 +629,9 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
     }
     if (p->tensor) {  // TENSOR strategy: the 2m taps of every node, in cell order
       const KernelSet<R>& ks = kernels_of<R>(p);
-      ks.taps1<<<(unsigned)((p->M + T1_THREADS - 1) / T1_THREADS), T1_THREADS, 0, st>>>(p->geom, poly_of<R>(p),
-                                                                                       (const R*)p->d_kc,
-                                                                                       (R*)p->d_wt);
+      CK(launch_k(ks.taps1, (unsigned)((p->M + T1_THREADS - 1) / T1_THREADS), T1_THREADS, 0, st, p->geom, WpnArg{p->wpn},
+                  (const R*)p->d_kc, (R*)p->d_wt));
       ++p->launches;
-      CKL();
     }
   } else if (p->use_bs) {
     TRY(launch_binsort<R>(p, st));
@@ -657,25 +687,25 @@ template <typename T>
 nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st) {
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
+  (void)wp;
+  const WpnArg wpn{p->wpn};
   const auto* grid = (const typename cplx<T>::type*)p->d_grid;
   if (p->cellmode && p->D >= 2) {
-    ks.interp_cell<<<dim3((unsigned)p->n_tiles, (unsigned)p->B), RC_THREADS, p->region_bytes, st>>>(
-        p->geom, wp, grid, (const T*)p->d_kc, p->d_jc, p->d_cstart, p->node_begin, p->node_end, f);
+    CK(launch_k(ks.interp_cell, dim3((unsigned)p->n_tiles, (unsigned)p->B), RC_THREADS, p->region_bytes, st, p->geom, wpn,
+                grid, (const T*)p->d_kc, (const int*)p->d_jc, (const int*)p->d_cstart, p->node_begin, p->node_end, f));
   } else if (p->use_ind) {
     ks.interp_nd<<<(unsigned)p->n_tiles, RN_THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
   } else if (p->cellmode && p->D == 1) {
-    const int sharded = p->node_begin > 0 || p->node_end < p->M;
-    static const int i1_ctas = getenv("NFFTB_I1_CTAS") ? atoi(getenv("NFFTB_I1_CTAS")) : 0;  // diagnostic
-    const unsigned gi = (unsigned)((p->M + I1_THREADS - 1) / I1_THREADS);
-    ks.interp1<<<i1_ctas > 0 ? std::min<unsigned>(gi, (unsigned)i1_ctas) : gi, I1_THREADS, 0, st>>>(
-        p->geom, wp, grid, (const T*)p->d_kc, p->d_jc, p->node_begin, p->node_end, sharded, f);
+    const unsigned segs = (unsigned)((p->Nt[0] + I1_SEG - 1) / I1_SEG);
+    CK(launch_k(ks.interp1, dim3(segs, (unsigned)p->B), I1_THREADS, p->r1_interp_bytes, st, p->geom, wpn, grid,
+                (const T*)p->d_kc, (const int*)p->d_jc, (const int*)p->d_cstart, p->node_begin, p->node_end, f));
   } else if (p->tiled) {
     ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
   } else {
-    ks.interp_direct<<<p->grid_direct, THREADS, 0, st>>>(p->geom, wp, grid, (const T*)p->d_ks, p->d_perm,
-                                                               p->node_begin, p->node_end, f);
+    CK(launch_k(ks.interp_direct, p->grid_direct, THREADS, 0, st, p->geom, wpn, grid, (const T*)p->d_ks,
+                (const int*)p->d_perm, p->node_begin, p->node_end, f));
   }
   ++p->launches;
   CKL();
@@ -718,36 +748,21 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   }
   if (p->cellmode && p->D >= 2) {
     rec(p, 1, 1);
-    ks.spread_cell<<<dim3((unsigned)p->n_tiles, (unsigned)p->B), 256, p->sc_bytes, st>>>(p->geom, wp, f, (const T*)p->d_kc, p->d_jc,
-                                                                  p->d_cstart, p->node_begin, p->node_end, p->sc_cap,
-                                                                  grid);
-    ++p->launches;
-    CKL();
-    return NFFT_SUCCESS;
-  }
-  if (p->cellmode && p->D == 1 && p->tensor) {
-    // TENSOR taps, thread per cell: every grid cell written exactly once, no zero pass
-    rec(p, 1, 1);
-    const int sharded = p->node_begin > 0 || p->node_end < p->M;
-    ks.spread1t<<<(unsigned)((p->Nt[0] + T1_THREADS - 1) / T1_THREADS), T1_THREADS, 0, st>>>(
-        p->geom, f, (const T*)p->d_wt, p->d_jc, p->d_cstart, p->node_begin, p->node_end, sharded, grid);
+    CK(launch_k(ks.spread_cell, dim3((unsigned)p->n_tiles, (unsigned)p->B), 256, p->sc_bytes, st, p->geom, WpnArg{p->wpn},
+                f, (const T*)p->d_kc, (const int*)p->d_jc, (const int*)p->d_cstart, p->node_begin, p->node_end, p->sc_cap,
+                grid));
     ++p->launches;
     CKL();
     return NFFT_SUCCESS;
   }
   if (p->cellmode && p->D == 1) {
-    // owner-computes: every grid cell written exactly once, no zero pass
+    // owner-computes segment gather (POLYNOMIAL or TENSOR taps): every grid cell written exactly once,
+    // no zero pass
     rec(p, 1, 1);
-    const int sharded = p->node_begin > 0 || p->node_end < p->M;
-    const int segs = (int)((p->Nt[0] + S1_SEG - 1) / S1_SEG);
-    // one resident wave, grid-stride over the segments: measured 56.5 -> 49.4 us per execute step (1D
-    // config 2), because the full-size grid kept every SM's shared memory busy and left no room for the
-    // concurrent direct NFFT's kernels; NFFTB_S1_CTAS overrides (diagnostic)
-    static const int s1_ctas = getenv("NFFTB_S1_CTAS") ? atoi(getenv("NFFTB_S1_CTAS")) : 0;
-    const unsigned gs = (unsigned)((segs + S1_WARPS - 1) / S1_WARPS);
-    const unsigned cap = s1_ctas > 0 ? (unsigned)s1_ctas : (unsigned)(p->sm_count * std::max(1, p->s1_occ));
-    ks.spread1<<<std::min<unsigned>(gs, cap), 32 * S1_WARPS, p->r1_spread_bytes, st>>>(
-        p->geom, wp, f, (const T*)p->d_kc, p->d_jc, p->d_cstart, p->node_begin, p->node_end, sharded, grid);
+    const unsigned segs = (unsigned)((p->Nt[0] + S1_SEG - 1) / S1_SEG);
+    CK(launch_k(p->tensor ? ks.spread1t : ks.spread1, dim3(segs, (unsigned)p->B), S1_THREADS, p->r1_spread_bytes, st,
+                p->geom, WpnArg{p->wpn}, f, (const T*)p->d_kc, (const T*)p->d_wt, (const int*)p->d_jc,
+                (const int*)p->d_cstart, p->node_begin, p->node_end, grid));
     ++p->launches;
     CKL();
     return NFFT_SUCCESS;
@@ -775,8 +790,8 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     ks.spread_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, f, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, grid);
   } else {
-    ks.spread_direct<<<p->grid_direct, THREADS, 0, st>>>(p->geom, wp, f, (const T*)p->d_ks, p->d_perm,
-                                                               p->node_begin, p->node_end, grid);
+    CK(launch_k(ks.spread_direct, p->grid_direct, THREADS, 0, st, p->geom, WpnArg{p->wpn}, f, (const T*)p->d_ks,
+                (const int*)p->d_perm, p->node_begin, p->node_end, grid));
   }
   ++p->launches;
   CKL();
@@ -1060,6 +1075,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   CK(cudaGetDeviceProperties(&prop, dev));
   const size_t smem_max = prop.sharedMemPerBlockOptin;
   bool tiled;
+#ifdef NFFTB_TILE_VARIANTS
   if (opt.method != NFFT_METHOD_AUTO && opt.method != NFFT_METHOD_DIRECT) {
     if (region_bytes > smem_max) return NFFT_ERROR_BAD_TILE;
     tiled = true;
@@ -1068,6 +1084,13 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   } else {
     tiled = region_bytes <= smem_max;
   }
+#else
+  // default build: cell mode (AUTO / TILED) with the unblocked kernels as the fallback; the
+  // first-generation tile-mode variants are compiled only with -DNFFTB_TILE_VARIANTS
+  if (opt.method > NFFT_METHOD_DIRECT) return NFFT_ERROR_UNSUPPORTED;
+  if (opt.method == NFFT_METHOD_TILED && region_bytes > smem_max) return NFFT_ERROR_BAD_TILE;
+  tiled = false;
+#endif
 
   nfft_plan p = new (std::nothrow) nfft_plan_s();
   if (!p) return NFFT_ERROR_OUT_OF_MEMORY;

@@ -1093,7 +1093,7 @@ __global__ void __launch_bounds__(THREADS) spread_gather_kernel(Geom g, WinPoly<
 
 // ------------------------------------------------------------ direct (unblocked)
 template <typename T, int D, int M, int DEG>
-__global__ void __launch_bounds__(THREADS) interp_direct_kernel(Geom g, WinPoly<T> wp,
+__global__ void __launch_bounds__(THREADS) interp_direct_kernel(Geom g, WinPolyN<T, D, M> wp,
                                                                 const typename cplx<T>::type* __restrict__ grid,
                                                                 const T* __restrict__ ks, const int* __restrict__ perm,
                                                                 int nb, int ne, typename cplx<T>::type* __restrict__ f) {
@@ -1169,7 +1169,7 @@ __global__ void __launch_bounds__(THREADS) interp_direct_kernel(Geom g, WinPoly<
 }
 
 template <typename T, int D, int M, int DEG>
-__global__ void __launch_bounds__(THREADS) spread_direct_kernel(Geom g, WinPoly<T> wp,
+__global__ void __launch_bounds__(THREADS) spread_direct_kernel(Geom g, WinPolyN<T, D, M> wp,
                                                                 const typename cplx<T>::type* __restrict__ f,
                                                                 const T* __restrict__ ks, const int* __restrict__ perm,
                                                                 int nb, int ne, typename cplx<T>::type* __restrict__ grid) {

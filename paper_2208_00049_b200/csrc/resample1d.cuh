@@ -28,255 +28,280 @@
 
 namespace nfftb {
 
-constexpr int I1_THREADS = 256;           // interp1c: one node per thread
-constexpr int S1_WARPS = 4;               // spread1c: warps per CTA
-constexpr int S1_K = 2;                   // spread1c: cells per lane
-constexpr int S1_SEG = 32 * S1_K;         // cells per warp
-constexpr int S1_CAP = 64;                // node slots per warp chunk (typical window: ~0.5 (SEG + 2m) nodes)
-
 
 // ---------------------------------------------------------------- forward
+// interp1s: one CTA per segment of S1_SEG consecutive cells (b = blockIdx.y),
+// the paper's block with its index set cached (Alg. 3): the
+// CTA's nodes are those of its cells, the cell-sorted range [cstart[y0],
+// cstart[y0 + SEG]); the grid cells they read are the block index set
+// [y0 - m + 1, y0 + SEG + m - 1]. The index set streams into shared memory
+// with cp.async (it depends only on y0) while the threads load their nodes'
+// coordinates and indices, so the two global-memory latencies overlap; then
+// every node evaluates its 2m taps (even/odd Horner) and sums the 2m cells
+// from shared memory, and its value is written to f[j] (caller's order).
+constexpr int I1_THREADS = 128;
+constexpr int I1_SEG = 512;               // cells per CTA
+constexpr int I1_U = 3;                   // nodes per thread loaded before the barrier
+
+__host__ __device__ inline size_t i1_smem_bytes(int M, size_t csize) {
+  return (((size_t)I1_SEG + 2 * M) * csize + 15) & ~(size_t)15;
+}
+
 template <typename T, int M, int DEG>
-__global__ void __launch_bounds__(I1_THREADS) interp1c_kernel(Geom g, WinPoly<T> wp,
+__global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T, 1, M> wp,
                                                               const typename cplx<T>::type* __restrict__ grid,
                                                               const T* __restrict__ kc, const int* __restrict__ jc,
-                                                              int nb, int ne, int sharded,
+                                                              const int* __restrict__ cstart, int nb, int ne,
                                                               typename cplx<T>::type* __restrict__ f) {
   using C = typename cplx<T>::type;
-  for (int pc = blockIdx.x * I1_THREADS + threadIdx.x; pc < g.M; pc += gridDim.x * I1_THREADS) {
-  if (sharded && (pc < nb || pc >= ne)) continue;  // shard = range of the cell-sorted order
-  const int j = jc[pc];
-  double frac;
+  constexpr int TAPS = 2 * M;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sg = reinterpret_cast<C*>(smem_raw);  // window cell e <-> binning cell y0 - m + 1 + e
+  NFFTB_TRACE(0);
   const int Nt = g.Nt[0];
-  const int c = node_cell((double)kc[pc], g.Ntd[0], Nt, frac);
-  T w[2 * M];
-  window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
-  // storage of the footprint's first cell: binning cell c = (a + Nt/2) mod Nt, storage (a - m + 1) mod Nt
-  int s0 = c - M + 1 - (Nt >> 1);
-  if (s0 < 0) s0 += Nt;
-  if (s0 < 0) s0 = pos_mod(s0, Nt);
-  int sl[2 * M];
-#pragma unroll
-  for (int l = 0; l < 2 * M; ++l) {
-    int s = s0 + l;
-    if (s >= Nt) s -= Nt;
-    if (s >= Nt) s = pos_mod(s, Nt);
-    sl[l] = s;
-  }
-  for (int b = 0; b < g.B; ++b) {
+  const int y0 = blockIdx.x * I1_SEG;
+  const int b = blockIdx.y;
+  const int nseg = min(I1_SEG, Nt - y0);
+  const int W = nseg + TAPS - 1;
+  // 1. the block index set -> shared memory (asynchronous; storage (cell - Nt/2) mod Nt)
+  {
     const C* gb = grid + (long long)b * g.grid_cells;
-    C v[2 * M];
+    int s0 = y0 - M + 1 - (Nt >> 1);
+    if (s0 < 0) s0 += Nt;
+    if (s0 < 0) s0 = pos_mod(s0, Nt);
+    for (int e = threadIdx.x; e < W; e += I1_THREADS) {
+      int s = s0 + e;
+      while (s >= Nt) s -= Nt;
+      cp_async_cell<T>(sg + e, gb + s);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  // 2. this CTA's nodes (cell-sorted range of its cells), clipped to the shard [nb, ne)
+  const int p0 = max(__ldg(cstart + y0), nb), p1 = min(__ldg(cstart + y0 + nseg), ne);
+  double kk[I1_U];
+  int jj[I1_U];
 #pragma unroll
-    for (int l = 0; l < 2 * M; ++l) v[l] = __ldg(gb + sl[l]);
+  for (int i = 0; i < I1_U; ++i) {
+    const int p = p0 + threadIdx.x + i * I1_THREADS;
+    jj[i] = -1;
+    if (p < p1) {
+      kk[i] = (double)kc[p];
+      jj[i] = jc[p];
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  NFFTB_TRACE(1);
+  C* fb = f + (long long)b * g.M;
+  auto one = [&](double k, int j) {
+    double frac;
+    const int c = node_cell(k, g.Ntd[0], Nt, frac);  // c in [y0, y0 + nseg): footprint starts at window cell c - y0
+    T w[TAPS];
+    window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
+    const C* row = sg + (c - y0);
     C acc;
     acc.x = (T)0;
     acc.y = (T)0;
 #pragma unroll
-    for (int l = 0; l < 2 * M; ++l) {
-      acc.x = fma(w[l], v[l].x, acc.x);
-      acc.y = fma(w[l], v[l].y, acc.y);
+    for (int l = 0; l < TAPS; ++l) {
+      const C v = row[l];
+      acc.x = fma(w[l], v.x, acc.x);
+      acc.y = fma(w[l], v.y, acc.y);
     }
-    f[(long long)b * g.M + j] = acc;
-  }
-  }  // nodes
+    fb[j] = acc;
+  };
+#pragma unroll
+  for (int i = 0; i < I1_U; ++i)
+    if (jj[i] >= 0) one(kk[i], jj[i]);
+  // dense segments: the remaining nodes
+  for (int p = p0 + threadIdx.x + I1_U * I1_THREADS; p < p1; p += I1_THREADS) one((double)kc[p], jc[p]);
+  NFFTB_TRACE(2);
 }
 
 // ---------------------------------------------------------------- adjoint
-// spread1c: one warp per segment of S1_SEG cells (owner-computes). The warp
-// stages the nodes of its WINDOW (cells [y0 - m, y0 + SEG + m - 2], i.e. every
-// node whose footprint reaches the segment; contiguous cell-sorted ranges from
-// cstart) and spreads them TAP-PARALLEL: the warp is split into groups of G =
-// 8 (m <= 4) or 16 lanes; a group takes one node, lane l evaluates tap l
-// (coefficients of its mirror pair in registers) and the tap is shuffled to
-// the lane that owns its cell: lane q always owns the cells i = q (mod G) of
-// the group's private shared-memory accumulator (no two lanes ever touch the
-// same cell: no conflict, no atomic, no barrier between nodes). The groups' copies are
-// summed when the segment's cells are written, each exactly once, with plain
-// coalesced stores (no zero pass, no halo merge: the paper's locked merge of
-// PAPER.md:578-582 becomes reading the halo NODES).
-template <int M>
-struct S1Cfg {
-  static constexpr int G = 2 * M <= 8 ? 8 : 16;   // lanes per node
-  static constexpr int NG = 32 / G;               // nodes per warp step = accumulator copies
-  static constexpr int NE = S1_SEG + 2 * M - 1;   // window cells (full segment)
-  static constexpr int LEN = NE + 2 * M - 1;      // accumulator cells: window cell e, tap l -> e + l
-};
+// spread1s: OWNER-COMPUTES gather, one CTA per segment of S1_SEG consecutive
+// cells (b = blockIdx.y). The nodes that reach the segment are those of the
+// window cells [y0 - m, y0 + SEG + m - 2]: ONE contiguous range of the
+// cell-sorted order (cstart; a wrapped window is a wrapped range, handled with
+// virtual positions V = cstart[c mod Nt] + M * floor(c / Nt)). The CTA
+//  1. reads the window's node range and each thread's reach from cstart
+//     (no shared table, no barrier),
+//  2. stages every window node once: its value f_j, its window cell and its
+//     2m taps (POLYNOMIAL: even/odd Horner of the window table,
+//     PAPER.md:628-642; TENSOR: the stored taps) in shared
+//     memory,
+//  3. every thread owns S1_K consecutive cells y and walks the nodes in reach
+//     (window cells [y - m, y + K + m - 2]: one contiguous slot range, so the
+//     walk is one loop without per-cell divergence); a node in window cell x
+//     adds f_j w_j[y - x + m - 1] to every owned cell y in its reach
+//     (predicated loads and FMAs, no branches),
+//  4. writes each of its cells once (plain stores: no atomics, no zero pass,
+//     no halo merge — the paper's locked merge of PAPER.md:578-582 becomes
+//     reading the halo NODES).
+// A window with more than S1_CAP nodes is processed in chunks (the
+// accumulators stay in registers).
+constexpr int S1_THREADS = 128;
+constexpr int S1_K = 4;                   // consecutive cells per thread
+constexpr int S1_SEG = S1_THREADS * S1_K; // 512 cells per CTA
+constexpr int S1_CAP = 320;               // staged nodes per chunk (mean ~0.5 (SEG + 2m) at M = N = Nt/2)
 
-// shared memory of one spread1c warp (host and device agree)
-__host__ __device__ inline size_t s1_warp_bytes(int M, size_t csize, size_t rsize) {
-  const int G = 2 * M <= 8 ? 8 : 16, NG = 32 / G;
-  const int NE = S1_SEG + 2 * M - 1, LEN = NE + 2 * M - 1;
-  size_t b = (size_t)NG * LEN * csize;                // accumulator copies
-  b += (size_t)S1_CAP * (csize + rsize);              // staged node: value, zeta
-  b += (size_t)S1_CAP * 4;                            // staged node: window cell
-  b += (size_t)(2 * NE + 2) * 4;                      // per window cell: first slot, position base
+// tap row pitch: 2m taps, odd pitch (neighbouring rows in distinct banks)
+__host__ __device__ constexpr int s1_pitch(int M) { return 2 * M + 1; }
+
+// shared memory of one spread1s CTA (host and device agree)
+__host__ __device__ inline size_t s1_smem_bytes(int M, size_t csize, size_t rsize) {
+  size_t b = (size_t)S1_CAP * csize;                       // staged values
+  b += (size_t)S1_CAP * s1_pitch(M) * rsize;               // staged tap rows
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)S1_CAP * 4;                                 // staged window cells
   return (b + 15) & ~(size_t)15;
 }
 
-template <typename T, int M, int DEG>
-__global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly<T> wp,
-                                                                 const typename cplx<T>::type* __restrict__ f,
-                                                                 const T* __restrict__ kc, const int* __restrict__ jc,
-                                                                 const int* __restrict__ cstart, int nb, int ne,
-                                                                 int sharded, typename cplx<T>::type* __restrict__ grid) {
+template <typename T, int M, int DEG, bool TENSOR>
+__global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T, 1, M> wp,
+                                                              const typename cplx<T>::type* __restrict__ f,
+                                                              const T* __restrict__ kc, const T* __restrict__ wt,
+                                                              const int* __restrict__ jc,
+                                                              const int* __restrict__ cstart, int nb, int ne,
+                                                              typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
-  using Cfg = S1Cfg<M>;
-  constexpr int TAPS = 2 * M, G = Cfg::G, NG = Cfg::NG, LEN = Cfg::LEN;
-  constexpr int PER = (Cfg::NE + 1 + 31) / 32;
+  constexpr int TAPS = 2 * M, TP = s1_pitch(M), REACH = S1_K + 2 * M - 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int Nt = g.Nt[0];
-  // grid-stride over the warp segments (the launch may use fewer CTAs than segments)
-  for (int wseg = blockIdx.x * S1_WARPS + warp;; wseg += gridDim.x * S1_WARPS) {
-  const int y0 = wseg * S1_SEG;
-  if (y0 >= Nt) break;
+  C* sval = reinterpret_cast<C*>(smem_raw);
+  T* stap = reinterpret_cast<T*>(sval + S1_CAP);
+  int* scel = reinterpret_cast<int*>(smem_raw + ((S1_CAP * sizeof(C) + (size_t)S1_CAP * TP * sizeof(T) + 15) & ~(size_t)15));
+  NFFTB_TRACE(0);
+  const int Nt = g.Nt[0], Mn = g.M;
+  const int y0 = blockIdx.x * S1_SEG;
+  const int b = blockIdx.y;
   const int nseg = min(S1_SEG, Nt - y0);
-  const int NE = nseg + 2 * M - 1;  // window cell e <-> binning cell (y0 - m + e) mod Nt
-  unsigned char* wb = smem_raw + (size_t)warp * s1_warp_bytes(M, sizeof(C), sizeof(T));
-  C* acc = reinterpret_cast<C*>(wb);                 // [NG][LEN]: cell y0 - 2m + 1 + i
-  C* sv = acc + NG * LEN;                            // [S1_CAP] node value
-  T* sz = reinterpret_cast<T*>(sv + S1_CAP);         // [S1_CAP] zeta = frac - 1/2
-  int* se = reinterpret_cast<int*>(sz + S1_CAP);     // [S1_CAP] window cell
-  int* ws = se + S1_CAP;                             // [NE + 1] first window slot of window cell e
-  int* wbase = ws + Cfg::NE + 1;                     // [NE] position of slot s of cell e = wbase[e] + s
-
-  // window slot starts: the lane's cstart loads issued together, warp scan of the counts
-  int total;
-  {
-    int c_lo[PER], c_hi[PER];
+  const int W = nseg + 2 * M - 1;  // window cell u <-> binning cell y0 - m + u
+  // 1. virtual position of the first node of window cell u (u = W: one past the window's last node)
+  auto vpos = [&](int u) {
+    int c = y0 - M + u, wrap = 0;  // c in (-Nt, 2 Nt): 2m < Nt
+    if (c < 0) {
+      c += Nt;
+      wrap = -1;
+    } else if (c >= Nt) {
+      c -= Nt;
+      wrap = 1;
+    }
+    return __ldg(cstart + c) + wrap * Mn;
+  };
+  // the window's node range (uniform) and this thread's reach: window cells [K t, K t + REACH)
+  const int t = threadIdx.x;
+  const int vbase = vpos(0), vend = vpos(W);
+  const int r_lo_v = vpos(min(S1_K * t, W)), r_hi_v = vpos(min(S1_K * t + REACH, W));
+  const int total = vend - vbase;
+  const int r_lo = r_lo_v - vbase, r_hi = r_hi_v - vbase;
+  C acc[S1_K];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = lane * PER + q;
-      c_lo[q] = c_hi[q] = 0;
-      if (e < NE) {
-        int c = y0 - M + e;
-        if (c < 0) c += Nt;
-        if (c >= Nt) c -= Nt;
-        if ((unsigned)c >= (unsigned)Nt) c = pos_mod(c, Nt);
-        c_lo[q] = __ldg(cstart + c);
-        c_hi[q] = __ldg(cstart + c + 1);
+  for (int k = 0; k < S1_K; ++k) {
+    acc[k].x = (T)0;
+    acc[k].y = (T)0;
+  }
+  const C* fb = f + (long long)b * Mn;
+  NFFTB_TRACE(1);
+  for (int clo = 0; clo < total; clo += S1_CAP) {
+    const int cnt = min(S1_CAP, total - clo);
+    if (clo > 0) __syncthreads();  // previous chunk's gathers are done
+    // 2. stage the chunk: coordinates and indices, then the values' loads are issued and the taps
+    //    (which need only the coordinates) are evaluated while they are in flight
+    constexpr int U = (S1_CAP + S1_THREADS - 1) / S1_THREADS;
+    int pp[U], jj[U], wv[U];
+    double kk[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const int q = threadIdx.x + i * S1_THREADS;
+      pp[i] = -1;
+      jj[i] = -1;
+      wv[i] = 0;
+      kk[i] = 0.0;
+      if (q < cnt) {
+        int p = vbase + clo + q;  // virtual position in (-M, 2M)
+        if (p < 0) {
+          p += Mn;
+          wv[i] = -1;
+        } else if (p >= Mn) {
+          p -= Mn;
+          wv[i] = 1;
+        }
+        pp[i] = p;
+        kk[i] = (double)kc[p];
+        jj[i] = (p >= nb && p < ne) ? __ldg(jc + p) : -1;  // node shard = range [nb, ne) of the cell order
       }
     }
-    int sum = 0;
+    C v[U];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) sum += c_hi[q] - c_lo[q];
-    int run = warp_exclusive_scan(sum, total);
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = lane * PER + q;
-      if (e <= NE) ws[e] = run;
-      if (e < NE) wbase[e] = c_lo[q] - run;
-      run += c_hi[q] - c_lo[q];
+    for (int i = 0; i < U; ++i) {
+      v[i].x = (T)0;
+      v[i].y = (T)0;
+#ifdef S1X_COALESCED_F
+      if (jj[i] >= 0) v[i] = fb[pp[i]];
+#else
+      if (jj[i] >= 0) v[i] = fb[jj[i]];
+#endif
     }
-  }
-  // tap of this lane and the coefficients of its mirror pair (w_l = E + zeta O, w_{2m-1-l} = E - zeta O)
-  const int grp = lane / G, l = lane % G;
-  const bool tap_on = l < TAPS;
-  const int lp = l < M ? l : (TAPS - 1 - l);
-  const T sgn = l < M ? (T)1 : (T)-1;
-  T ce[DEG / 2 + 1], co[(DEG + 1) / 2];
 #pragma unroll
-  for (int z = 0; z <= DEG; ++z) {
-    const T c = tap_on ? wp.mu[0][lp < M ? lp : 0][z] : (T)0;
-    if (z % 2 == 0) ce[z / 2] = c;
-    else co[z / 2] = c;
-  }
-  __syncwarp();
-  const int sy0 = pos_mod(y0 - (Nt >> 1), Nt);  // storage of binning cell y0
-  for (int b = 0; b < g.B; ++b) {
-    for (int i = lane; i < NG * LEN; i += 32) {
-      acc[i].x = (T)0;
-      acc[i].y = (T)0;
+    for (int i = 0; i < U; ++i) {
+      const int q = threadIdx.x + i * S1_THREADS;
+      if (pp[i] < 0) continue;
+      double frac;
+      const int c = node_cell(kk[i], g.Ntd[0], Nt, frac);
+      scel[q] = c + wv[i] * Nt - (y0 - M);  // window cell (virtual cell of the virtual position)
+      T w[TAPS];
+      if constexpr (TENSOR) {
+#pragma unroll
+        for (int l = 0; l < TAPS; ++l) w[l] = __ldg(wt + (long long)pp[i] * TAPS + l);
+      } else {
+#ifdef S1X_NO_TAPS
+#pragma unroll
+        for (int l = 0; l < TAPS; ++l) w[l] = (T)frac;
+#else
+        window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
+#endif
+      }
+      T* row = stap + q * TP;
+#pragma unroll
+      for (int l = 0; l < TAPS; ++l) row[l] = w[l];
     }
-    for (int clo = 0; clo < max(total, 1); clo += S1_CAP) {
-      const int chi = min(total, clo + S1_CAP);
-      // stage the chunk: window cell, zeta and value of every slot (loads of all the lane's slots in flight)
-      constexpr int SPL = (S1_CAP + 31) / 32;
-      int jj[SPL], ee[SPL];
-      double kk[SPL];
 #pragma unroll
-      for (int u = 0; u < SPL; ++u) {
-        const int sl = clo + lane + 32 * u;
-        jj[u] = -1;
-        ee[u] = -1;
-        if (sl < chi) {
-          int lo = 0, hi = NE;  // window cell of the slot: last e with ws[e] <= sl
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (ws[mid] <= sl) lo = mid;
-            else hi = mid;
-          }
-          const int pc = wbase[lo] + sl;
-          ee[u] = lo;
-          jj[u] = (sharded && (pc < nb || pc >= ne)) ? -1 : jc[pc];  // shard = range of the cell order
-          kk[u] = (double)kc[pc];
+    for (int i = 0; i < U; ++i)
+      if (pp[i] >= 0) sval[threadIdx.x + i * S1_THREADS] = v[i];
+    NFFTB_TRACE(2);
+    __syncthreads();
+    NFFTB_TRACE(3);
+    // 3. owner-computes gather: node in window cell K t + v adds to cell K t + k with tap
+    //    l = k - v + 2m - 1 when 0 <= l < 2m
+    const int lo = max(r_lo - clo, 0), hi = min(r_hi - clo, cnt);
+    for (int q = lo; q < hi; ++q) {
+      const C val = sval[q];
+      const int l0 = TAPS - 1 - (scel[q] - S1_K * t);
+      const T* wr = stap + q * TP;
+#pragma unroll
+      for (int k = 0; k < S1_K; ++k) {
+        const int l = l0 + k;
+        if ((unsigned)l < (unsigned)TAPS) {
+          const T wk = wr[l];
+          acc[k].x = fma(wk, val.x, acc[k].x);
+          acc[k].y = fma(wk, val.y, acc[k].y);
         }
       }
-#pragma unroll
-      for (int u = 0; u < SPL; ++u) {
-        const int sl = lane + 32 * u;
-        if (ee[u] >= 0) {
-          C v;
-          v.x = (T)0;
-          v.y = (T)0;
-          if (jj[u] >= 0) v = f[(long long)b * g.M + jj[u]];
-          double frac;
-          node_cell(kk[u], g.Ntd[0], Nt, frac);
-          sv[sl] = v;
-          sz[sl] = (T)(frac - 0.5);
-          se[sl] = ee[u];
-        }
-      }
-      __syncwarp();
-      // tap-parallel accumulation: group grp takes slots grp, grp + NG, ...; lane l evaluates tap l,
-      // and the tap is handed (shuffle) to the lane q = (e + t) mod G that always owns the
-      // accumulator cells i = q (mod G): no two lanes ever update the same cell, no barrier.
-      C* my = acc + grp * LEN;
-      const int n = chi - clo;
-      const int q = l;
-#pragma unroll 2
-      for (int base = 0; base < n; base += NG) {  // uniform trip count (shuffles below)
-        const int sl = min(base + grp, n - 1);
-        const bool valid = base + grp < n;
-        const T zeta = sz[sl];
-        const C v = sv[sl];
-        const int e = se[sl];
-        const T z2 = zeta * zeta;
-        T ev = ce[DEG / 2];
-#pragma unroll
-        for (int z = DEG / 2 - 1; z >= 0; --z) ev = fma(ev, z2, ce[z]);
-        T od = co[(DEG - 1) / 2];
-#pragma unroll
-        for (int z = (DEG - 1) / 2 - 1; z >= 0; --z) od = fma(od, z2, co[z]);
-        const T w = fma(sgn * zeta, od, ev);
-        const int t = (q - e) & (G - 1);
-        const T wt = __shfl_sync(0xffffffffu, w, grp * G + t);
-        if (valid && t < TAPS) {
-          C a = my[e + t];
-          a.x = fma(wt, v.x, a.x);
-          a.y = fma(wt, v.y, a.y);
-          my[e + t] = a;
-        }
-      }
-      __syncwarp();
     }
-    // cell y0 + y <-> accumulator index y + 2m - 1; sum the group copies, one coalesced store per cell
-    C* dst = grid + (long long)b * g.grid_cells;
-    for (int y = lane; y < nseg; y += 32) {
-      C a = acc[y + TAPS - 1];
-#pragma unroll
-      for (int q = 1; q < NG; ++q) {
-        const C c = acc[q * LEN + y + TAPS - 1];
-        a.x += c.x;
-        a.y += c.y;
-      }
-      int s = sy0 + y;
-      if (s >= Nt) s -= Nt;
-      dst[s] = a;
-    }
-    __syncwarp();
   }
-  }  // segments
+  NFFTB_TRACE(4);
+  // 4. one plain store per owned cell (binning cell y <-> storage (y - Nt/2) mod Nt)
+  C* dst = grid + (long long)b * g.grid_cells;
+  int s = y0 + S1_K * t - (Nt >> 1);
+  if (s < 0) s += Nt;
+#pragma unroll
+  for (int k = 0; k < S1_K; ++k) {
+    if (S1_K * t + k < nseg) {
+      int sk = s + k;
+      if (sk >= Nt) sk -= Nt;
+      dst[sk] = acc[k];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- TENSOR precompute (D = 1)
@@ -287,7 +312,7 @@ __global__ void __launch_bounds__(32 * S1_WARPS) spread1c_kernel(Geom g, WinPoly
 constexpr int T1_THREADS = 256;
 
 template <typename T, int M, int DEG>
-__global__ void __launch_bounds__(T1_THREADS) taps1_kernel(Geom g, WinPoly<T> wp, const T* __restrict__ kc,
+__global__ void __launch_bounds__(T1_THREADS) taps1_kernel(Geom g, WinPolyN<T, 1, M> wp, const T* __restrict__ kc,
                                                            T* __restrict__ wt) {
   const int pc = blockIdx.x * T1_THREADS + threadIdx.x;
   if (pc >= g.M) return;
@@ -297,54 +322,6 @@ __global__ void __launch_bounds__(T1_THREADS) taps1_kernel(Geom g, WinPoly<T> wp
   window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
 #pragma unroll
   for (int t = 0; t < 2 * M; ++t) wt[(long long)pc * 2 * M + t] = w[t];
-}
-
-// spread1t: adjoint with TENSOR taps, one thread per grid cell y (owner-computes
-// gather, every cell written exactly once, no shared memory): the nodes of
-// cells x = y - m + i, i = 0..2m-1, are the cell-sorted ranges [cstart[x],
-// cstart[x + 1]) and contribute f_j wt[pos][2m - 1 - i] (static tap index).
-template <typename T, int M>
-__global__ void __launch_bounds__(T1_THREADS) spread1t_kernel(Geom g, const typename cplx<T>::type* __restrict__ f,
-                                                              const T* __restrict__ wt, const int* __restrict__ jc,
-                                                              const int* __restrict__ cstart, int nb, int ne,
-                                                              int sharded, typename cplx<T>::type* __restrict__ grid) {
-  using C = typename cplx<T>::type;
-  constexpr int TAPS = 2 * M;
-  const int y = blockIdx.x * T1_THREADS + threadIdx.x;
-  const int Nt = g.Nt[0];
-  if (y >= Nt) return;
-  int lo[TAPS], hi[TAPS];
-#pragma unroll
-  for (int i = 0; i < TAPS; ++i) {
-    int x = y - M + i;  // binning cell of the i-th contributing cell
-    if (x < 0) x += Nt;
-    if (x >= Nt) x -= Nt;
-    if ((unsigned)x >= (unsigned)Nt) x = pos_mod(x, Nt);
-    lo[i] = __ldg(cstart + x);
-    hi[i] = __ldg(cstart + x + 1);
-    if (sharded) {  // shard = range [nb, ne) of the cell order
-      lo[i] = max(lo[i], nb);
-      hi[i] = min(hi[i], ne);
-    }
-  }
-  int s = y - (Nt >> 1);  // storage of binning cell y
-  if (s < 0) s += Nt;
-  for (int b = 0; b < g.B; ++b) {
-    const C* fb = f + (long long)b * g.M;
-    C acc;
-    acc.x = (T)0;
-    acc.y = (T)0;
-#pragma unroll
-    for (int i = 0; i < TAPS; ++i) {
-      for (int p = lo[i]; p < hi[i]; ++p) {
-        const T w = __ldg(wt + (long long)p * TAPS + (TAPS - 1 - i));
-        const C v = fb[__ldg(jc + p)];
-        acc.x = fma(w, v.x, acc.x);
-        acc.y = fma(w, v.y, acc.y);
-      }
-    }
-    grid[(long long)b * g.grid_cells + s] = acc;
-  }
 }
 
 }  // namespace nfftb

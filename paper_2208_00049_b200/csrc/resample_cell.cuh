@@ -38,7 +38,7 @@ constexpr int SC_K = 4;          // spread_cell: consecutive last-dimension cell
 
 // ---------------------------------------------------------------- forward
 template <typename T, int D, int M, int DEG>
-__global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel(Geom g, WinPoly<T> wp,
+__global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel(Geom g, WinPolyN<T, D, M> wp,
                                                                  const typename cplx<T>::type* __restrict__ grid,
                                                                  const T* __restrict__ kc, const int* __restrict__ jc,
                                                                  const int* __restrict__ cstart, int nb, int ne,
@@ -230,7 +230,7 @@ __host__ __device__ inline size_t spread_cell_smem_bytes(int D, int M, int rsize
 }
 
 template <typename T, int D, int M, int DEG>
-__global__ void __launch_bounds__(256) spread_cell_kernel(Geom g, WinPoly<T> wp,
+__global__ void __launch_bounds__(256) spread_cell_kernel(Geom g, WinPolyN<T, D, M> wp,
                                                           const typename cplx<T>::type* __restrict__ f,
                                                           const T* __restrict__ kc, const int* __restrict__ jc,
                                                           const int* __restrict__ cstart, int nb, int ne, int cap,

@@ -104,7 +104,7 @@ __host__ __device__ inline size_t rb_smem_bytes(int M, int rsize) {
 // cl (optional): the last-dimension binning cell of every position.
 constexpr int TN_NODES = 64;
 template <typename T, int D, int M, int DEG>
-__global__ void __launch_bounds__(TN_NODES) taps_nd_kernel(Geom g, WinPoly<T> wp, const T* __restrict__ kc,
+__global__ void __launch_bounds__(TN_NODES) taps_nd_kernel(Geom g, WinPolyN<T, D, M> wp, const T* __restrict__ kc,
                                                            T* __restrict__ wt, int* __restrict__ cl) {
   constexpr int ROW = D * 2 * M, RS = ROW + 1;
   __shared__ T s[TN_NODES * RS];
