@@ -133,28 +133,38 @@ def _footprints(nodes, geom):
 def resample_forward(ghat, nodes, geom):
     """Alg. 1 lines 7-9, the sum of eq. (SumOverNode)
     PAPER.md:482: f_j = sum_{l in I_{Ntilde,m}(k_j)} ghat_l psi~(k_j - l/Ntilde),
-    with psi~(k - l/Ntilde) = prod_d psi_hat_Base((Ntilde_d k_d - l_d)/m)."""
+    with psi~(k - l/Ntilde) = prod_d psi_hat_Base((Ntilde_d k_d - l_d)/m).
+    ghat may carry a leading batch axis (B vectors on the same nodes): the
+    footprint and taps are evaluated once and applied to every vector (the
+    per-vector arithmetic is unchanged); the result is then (B, M)."""
     nodes = np.asarray(nodes, np.float64).reshape(-1, geom["D"])
-    flat_grid = np.asarray(ghat, np.complex128).reshape(-1)
-    f = np.zeros(nodes.shape[0], dtype=np.complex128)
+    ghat = np.asarray(ghat, np.complex128)
+    batched = ghat.ndim == geom["D"] + 1
+    grid_t = np.ascontiguousarray(ghat.reshape(ghat.shape[0] if batched else 1, -1).T)  # (cells, B)
+    f_t = np.zeros((nodes.shape[0], grid_t.shape[1]), dtype=np.complex128)
     for flat, w in _footprints(nodes, geom):
-        f += w * flat_grid[flat]
-    return f
+        f_t += w[:, None] * grid_t[flat]
+    return f_t.T.copy() if batched else f_t[:, 0].copy()
 
 
 def resample_adjoint(f, nodes, geom):
     """Alg. 2 lines 1-3 in the node-outer evaluation order
     the paper prescribes: ghat_l += f_j psi~(k_j - l/Ntilde) for
-    every l in I_{Ntilde,m}(k_j)."""
+    every l in I_{Ntilde,m}(k_j). f may be (B, M) (B vectors on the same nodes,
+    footprints and taps shared); the result is then (B, *Ntilde)."""
     nodes = np.asarray(nodes, np.float64).reshape(-1, geom["D"])
-    f = np.asarray(f, np.complex128).reshape(-1)
+    f = np.asarray(f, np.complex128)
+    batched = f.ndim == 2
+    fb = f if batched else f.reshape(1, -1)
     size = int(np.prod(geom["Ntilde"]))
-    re = np.zeros(size)
-    im = np.zeros(size)
+    re = np.zeros((fb.shape[0], size))
+    im = np.zeros((fb.shape[0], size))
     for flat, w in _footprints(nodes, geom):
-        re += np.bincount(flat, weights=w * f.real, minlength=size)
-        im += np.bincount(flat, weights=w * f.imag, minlength=size)
-    return (re + 1j * im).reshape(geom["Ntilde"])
+        for b in range(fb.shape[0]):
+            re[b] += np.bincount(flat, weights=w * fb[b].real, minlength=size)
+            im[b] += np.bincount(flat, weights=w * fb[b].imag, minlength=size)
+    out = (re + 1j * im).reshape((fb.shape[0],) + tuple(geom["Ntilde"]))
+    return out if batched else out[0]
 
 
 def forward(nodes, fhat, N, m, sigma, rows=None, window_points="2m"):
@@ -170,12 +180,8 @@ def forward(nodes, fhat, N, m, sigma, rows=None, window_points="2m"):
     fhat = np.asarray(fhat, np.complex128)
     batched = fhat.ndim == geom["D"] + 1
     fb = fhat if batched else fhat[None]
-    out = []
-    for b in range(fb.shape[0]):
-        g = deconvolve_pad(fb[b], geom)
-        ghat = fft_forward(g)
-        out.append(resample_forward(ghat, nodes, geom))
-    out = np.stack(out)
+    ghat = np.stack([fft_forward(deconvolve_pad(fb[b], geom)) for b in range(fb.shape[0])])
+    out = resample_forward(ghat, nodes, geom)
     return out if batched else out[0]
 
 
@@ -189,10 +195,6 @@ def adjoint(nodes, f, N, m, sigma, window_points="2m"):
     f = np.asarray(f, np.complex128)
     batched = f.ndim == 2
     fb = f if batched else f[None]
-    out = []
-    for b in range(fb.shape[0]):
-        ghat = resample_adjoint(fb[b], nodes, geom)
-        g = fft_adjoint(ghat)
-        out.append(crop_deconvolve(g, geom))
-    out = np.stack(out)
+    ghat = resample_adjoint(fb, nodes, geom)
+    out = np.stack([crop_deconvolve(fft_adjoint(ghat[b]), geom) for b in range(fb.shape[0])])
     return out if batched else out[0]

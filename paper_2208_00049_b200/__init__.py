@@ -154,6 +154,11 @@ class NfftPlan:
         if stream is None and torch.cuda.is_available():
             stream = torch.cuda.current_stream(self.device).cuda_stream
         self.stream = stream
+        # the plan stream as a torch stream (for ordering against the caller's current stream)
+        self._pstream = None
+        if torch.cuda.is_available():
+            self._pstream = (torch.cuda.default_stream(self.device) if not stream
+                             else torch.cuda.ExternalStream(stream, device=self.device))
         nodes = self._nodes_arg(nodes)
         self.M = int(nodes.shape[0])
         opt = Options()
@@ -212,6 +217,30 @@ class NfftPlan:
         torch = _torch()
         return torch.empty(shape, dtype=self.tdtype_c, device=ref.device)
 
+    def _enter(self, *tensors):
+        """The library enqueues on the plan stream; when the caller's current
+        stream is another one, the plan stream first waits for it (inputs written
+        there are complete). Returns the caller's stream (or None)."""
+        if self._pstream is None or not any(getattr(t, "is_cuda", False) for t in tensors):
+            return None
+        torch = _torch()
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream == self._pstream.cuda_stream:
+            return None
+        self._pstream.wait_stream(cur)
+        return cur
+
+    def _exit(self, cur, *tensors):
+        """...and afterwards the caller's stream waits for the plan stream, and the
+        tensors the call used are marked as in use on it (the caching allocator
+        then does not hand temporaries to another allocation too early)."""
+        if cur is None:
+            return
+        cur.wait_stream(self._pstream)
+        for t in tensors:
+            if getattr(t, "is_cuda", False):
+                t.record_stream(self._pstream)
+
     # -- ABI calls -----------------------------------------------------------
     def set_nodes(self, nodes):
         nodes = self._nodes_arg(nodes)
@@ -229,7 +258,9 @@ class NfftPlan:
         fhat = self._data_arg(fhat, self._grid_shape())
         if out is None:
             out = self._empty_like_kind(fhat, (self.batch, self.M))
+        cur = self._enter(fhat, out)
         _check(lib().nfft_forward(self._h, _ptr(fhat), _ptr(out)), "nfft_forward")
+        self._exit(cur, fhat, out)
         return out
 
     def adjoint(self, f, out=None):
@@ -237,13 +268,17 @@ class NfftPlan:
         f = self._data_arg(f, (self.batch, self.M))
         if out is None:
             out = self._empty_like_kind(f, self._grid_shape())
+        cur = self._enter(f, out)
         _check(lib().nfft_adjoint(self._h, _ptr(f), _ptr(out)), "nfft_adjoint")
+        self._exit(cur, f, out)
         return out
 
     def run_stage(self, stage, inp=None, out=None):
         """One stage of Alg. 1/2 on device tensors (nfft_run_stage)."""
+        cur = self._enter(inp, out)
         _check(lib().nfft_run_stage(self._h, STAGES[stage], None if inp is None else _ptr(inp),
                                     None if out is None else _ptr(out)), f"nfft_run_stage({stage})")
+        self._exit(cur, inp, out)
         if stage == "precompute":
             self.precomputed = True
         return out
@@ -264,9 +299,11 @@ class NfftPlan:
             f_in = self._data_arg(f_in, (self.batch, self.M))
             if y_out is None:
                 y_out = torch.empty(self._grid_shape(), dtype=self.tdtype_c, device=f_in.device)
+        cur = self._enter(fhat, f_out, f_in, y_out)
         _check(lib().nfft_execute(self._h, flags, None if fhat is None else _ptr(fhat),
                                   None if f_out is None else _ptr(f_out), None if f_in is None else _ptr(f_in),
                                   None if y_out is None else _ptr(y_out)), "nfft_execute")
+        self._exit(cur, fhat, f_out, f_in, y_out)
         if precompute:
             self.precomputed = True
         return f_out, y_out

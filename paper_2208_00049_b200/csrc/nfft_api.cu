@@ -514,10 +514,8 @@ void configure_binsort(nfft_plan p) {
   // smallest grid that still gives every SM one CTA wins (measured on B200,
   // M = 2^18: 512 CTAs 68 us, 256 CTAs 37 us, 128 CTAs 25 us, 64 CTAs 32 us
   // per precompute stage including the graph launch).
-  const char* env = getenv("NFFTB_BS_RR");  // diagnostics: force one rounds-per-warp value
   int best_rr = 0, best_g = 0, best_over = 1 << 30;
   for (int rr : {1, 2, 4, 8}) {
-    if (env && rr != atoi(env)) continue;
     void* fn = binsort_fn_rr<R>(rr, p->D);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
       cudaGetLastError();
@@ -574,27 +572,15 @@ nfft_status cell_sort_d(nfft_plan p, cudaStream_t st) {
   const int M = (int)p->M;
   const int nc = (int)p->ncells;
   const int ntiles = (nc + CL_SCAN_TILE - 1) / CL_SCAN_TILE;
-  // NFFTB_PRE_CTAS caps the node-parallel kernels' grids (grid-stride; diagnostic)
-  static const int pre_ctas = getenv("NFFTB_PRE_CTAS") ? atoi(getenv("NFFTB_PRE_CTAS")) : 0;
-  unsigned gm = (unsigned)((std::max(M, ntiles) + CL_THREADS - 1) / CL_THREADS);
-  unsigned gp = (unsigned)((M + CL_THREADS - 1) / CL_THREADS);
-  if (pre_ctas > 0) {
-    gm = std::min<unsigned>(gm, (unsigned)pre_ctas);
-    gp = std::min<unsigned>(gp, (unsigned)pre_ctas);
-  }
-  static const int stop = getenv("NFFTB_DIAG_PRE_STOP") ? atoi(getenv("NFFTB_DIAG_PRE_STOP")) : 4;  // diagnostic
-  if (stop < 1) return NFFT_SUCCESS;
+  const unsigned gm = (unsigned)((std::max(M, ntiles) + CL_THREADS - 1) / CL_THREADS);
+  const unsigned gp = (unsigned)((M + CL_THREADS - 1) / CL_THREADS);
   cl_count_kernel<R, D><<<gm, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_ccount, p->d_cslot, p->d_err,
                                                    p->d_scan_status, ntiles, p->d_ctr);
-  if (stop < 2) return NFFT_SUCCESS;
   cl_scan_kernel<<<(unsigned)ntiles, CL_SCAN_THREADS, 0, st>>>(p->d_ccount, nc, p->d_scan_status, p->d_ctr,
                                                                p->d_cstart);
-  if (stop < 3) return NFFT_SUCCESS;
   cl_place_kernel<R, D><<<gp, CL_THREADS, 0, st>>>((const R*)p->d_nodes, p->geom, p->d_cslot, p->d_cstart,
                                                    (R*)p->d_kc, p->d_jc, p->d_ctr, p->d_big);
-  if (stop < 4) return NFFT_SUCCESS;
-  const unsigned gf = (unsigned)std::min<int64_t>((nc + CL_THREADS - 1) / CL_THREADS,
-                                                  pre_ctas > 0 ? pre_ctas : p->sm_count * 8);
+  const unsigned gf = (unsigned)std::min<int64_t>((nc + CL_THREADS - 1) / CL_THREADS, p->sm_count * 8);
   cl_fix_kernel<R, D><<<gf, CL_THREADS, 0, st>>>(p->geom, p->d_cstart, (R*)p->d_kc, p->d_jc, nc, p->d_ctr, p->d_big,
                                                  p->d_cslot, (R*)p->d_ks);
   p->launches += 4;
@@ -759,7 +745,8 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     // owner-computes segment gather (POLYNOMIAL or TENSOR taps): every grid cell written exactly once,
     // no zero pass
     rec(p, 1, 1);
-    const unsigned segs = (unsigned)((p->Nt[0] + S1_SEG - 1) / S1_SEG);
+    const unsigned segs = std::min<unsigned>((unsigned)((p->Nt[0] + S1_SEG - 1) / S1_SEG),
+                                             (unsigned)(S1_CTAS_PER_SM * p->sm_count));
     CK(launch_k(p->tensor ? ks.spread1t : ks.spread1, dim3(segs, (unsigned)p->B), S1_THREADS, p->r1_spread_bytes, st,
                 p->geom, WpnArg{p->wpn}, f, (const T*)p->d_kc, (const T*)p->d_wt, (const int*)p->d_jc,
                 (const int*)p->d_cstart, p->node_begin, p->node_end, grid));
@@ -975,12 +962,11 @@ nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, 
 
 // nfft_execute: the precompute and the adjoint chain (spread -> FFT -> crop) form the critical
 // path, so their internal streams get the highest priority (their CTAs are scheduled first when
-// they compete with the direct NFFT); NFFTB_ADJ_PRIORITY=0 keeps the default priority (diagnostic).
+// they compete with the direct NFFT; measured neutral to slightly positive, 1D config 2).
 static int adj_priority() {
   int lo = 0, hi = 0;
   if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return 0;
-  const char* e = getenv("NFFTB_ADJ_PRIORITY");
-  return (e && atoi(e) == 0) ? lo : hi;
+  return hi;
 }
 
 nfft_status copy_nodes(nfft_plan p, const void* nodes) {
@@ -1058,15 +1044,31 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   // dimension is padded for the bank-rotated interp loop (C128: TP - 1 readable cells, pitch % 8 == 0)
   int64_t Lreg[3] = {1, 1, 1};
   size_t region_cells = 1;
-  for (int d = 0; d < D; ++d) {
-    Lreg[d] = Q[d] + 2 * m - 1;
-    if (d == D - 1 && precision == NFFT_COMPLEX128) {
-      const int64_t tp = 2 * m <= 8 ? 8 : 16;
-      Lreg[d] = ((Q[d] + tp - 1) + 7) / 8 * 8;
+  auto region_of = [&]() {
+    region_cells = 1;
+    for (int d = 0; d < D; ++d) {
+      Lreg[d] = Q[d] + 2 * m - 1;
+      if (d == D - 1 && precision == NFFT_COMPLEX128) {
+        const int64_t tp = 2 * m <= 8 ? 8 : 16;
+        Lreg[d] = ((Q[d] + tp - 1) + 7) / 8 * 8;
+      }
+      region_cells *= (size_t)Lreg[d];
     }
-    region_cells *= (size_t)Lreg[d];
+    return region_cells * csz;
+  };
+  size_t region_bytes = region_of();
+  // default tiles with a large window (m >= 6 in 3D): halve the largest leading tile extent until the
+  // interpolation's staged region fits 200 KB of shared memory (e.g. 3D m = 7: 8 x 8 x 16 -> 4 x 8 x 16)
+  const bool default_tile = D >= 2 && opt.tile[0] == 0 && opt.tile[1] == 0 && opt.tile[2] == 0;
+  while (default_tile && region_bytes > 200 * 1024) {
+    int dm = -1;
+    for (int d = 0; d < D - 1; ++d)
+      if (Q[d] > 1 && (dm < 0 || Q[d] > Q[dm])) dm = d;
+    if (dm < 0) break;
+    Q[dm] = (Q[dm] + 1) / 2;
+    P[dm] = (Nt[dm] + Q[dm] - 1) / Q[dm];
+    region_bytes = region_of();
   }
-  const size_t region_bytes = region_cells * csz;
 
   DeviceGuard guard(opt.device);
   int dev = 0;
@@ -1189,15 +1191,14 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   // 2D batches of >= 8 transforms: row-segment adjoint with lanes = batch vectors (not for node
   // shards; the 16 + 2m - 1 window columns must not wrap onto themselves)
   p->batchmode = p->cellmode && D == 2 && p->B >= 8 && opt.node_begin == 0 && (opt.node_end == 0 || opt.node_end == M) &&
-                 Nt[1] >= RB_SEG + 2 * m - 1 && !getenv("NFFTB_NO_BATCH_KERNELS");
+                 Nt[1] >= RB_SEG + 2 * m - 1;
   p->bp = (int)((p->B + 31) / 32 * 32);
   if (ok && p->batchmode)
     ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && alloc(&p->d_wt, (size_t)M * D * 2 * m * rs) &&
          alloc((void**)&p->d_inv, (size_t)M * 4);
   // D = 2, 3 (not batched): warp-block adjoint over the TENSOR taps; the last-dimension window
   // (32 or 8 lanes + 2m - 1 cells) must not wrap onto itself
-  p->wbmode = p->cellmode && !p->batchmode && D >= 2 && Nt[D - 1] >= (D == 3 ? 8 : 32) + 2 * m - 1 &&
-              !getenv("NFFTB_NO_WB");
+  p->wbmode = p->cellmode && !p->batchmode && D >= 2 && Nt[D - 1] >= (D == 3 ? 8 : 32) + 2 * m - 1;
   if (ok && p->wbmode)
     ok = alloc(&p->d_wt, (size_t)M * D * 2 * m * rs) && alloc(&p->d_fc, (size_t)M * p->B * csz) &&
          alloc((void**)&p->d_cl, (size_t)M * 4);

@@ -59,8 +59,11 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
   C* sg = reinterpret_cast<C*>(smem_raw);  // window cell e <-> binning cell y0 - m + 1 + e
   NFFTB_TRACE(0);
   const int Nt = g.Nt[0];
-  const int y0 = blockIdx.x * I1_SEG;
   const int b = blockIdx.y;
+  const int nsegs = (Nt + I1_SEG - 1) / I1_SEG;
+  // grid-stride over the segments (the launch may use fewer CTAs than segments)
+  for (int sgi = blockIdx.x; sgi < nsegs; sgi += gridDim.x) {
+  const int y0 = sgi * I1_SEG;
   const int nseg = min(I1_SEG, Nt - y0);
   const int W = nseg + TAPS - 1;
   // 1. the block index set -> shared memory (asynchronous; storage (cell - Nt/2) mod Nt)
@@ -115,6 +118,8 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
     if (jj[i] >= 0) one(kk[i], jj[i]);
   // dense segments: the remaining nodes
   for (int p = p0 + threadIdx.x + I1_U * I1_THREADS; p < p1; p += I1_THREADS) one((double)kc[p], jc[p]);
+  __syncthreads();  // the next segment overwrites the staged index set
+  }  // segments
   NFFTB_TRACE(2);
 }
 
@@ -144,6 +149,10 @@ constexpr int S1_THREADS = 128;
 constexpr int S1_K = 4;                   // consecutive cells per thread
 constexpr int S1_SEG = S1_THREADS * S1_K; // 512 cells per CTA
 constexpr int S1_CAP = 320;               // staged nodes per chunk (mean ~0.5 (SEG + 2m) at M = N = Nt/2)
+// resident CTAs per SM of the spread launch (grid-stride over the segments). Measured on B200 in the
+// bench step (direct || adjoint NFFT, 1D 2^18, m = 4): 4 per SM 45.3 us, 5: 46.0, 6: 46.4, one CTA per
+// segment (7 resident): 54.1 us -- a full grid of spread CTAs keeps the concurrent forward FFT off the SMs.
+constexpr int S1_CTAS_PER_SM = 4;
 
 // tap row pitch: 2m taps, odd pitch (neighbouring rows in distinct banks)
 __host__ __device__ constexpr int s1_pitch(int M) { return 2 * M + 1; }
@@ -172,8 +181,12 @@ __global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T
   int* scel = reinterpret_cast<int*>(smem_raw + ((S1_CAP * sizeof(C) + (size_t)S1_CAP * TP * sizeof(T) + 15) & ~(size_t)15));
   NFFTB_TRACE(0);
   const int Nt = g.Nt[0], Mn = g.M;
-  const int y0 = blockIdx.x * S1_SEG;
   const int b = blockIdx.y;
+  const int nsegs = (Nt + S1_SEG - 1) / S1_SEG;
+  // grid-stride over the segments (the launch may use fewer CTAs than segments)
+  for (int sgi = blockIdx.x; sgi < nsegs; sgi += gridDim.x) {
+  if (sgi != (int)blockIdx.x) __syncthreads();  // the previous segment's gathers are done
+  const int y0 = sgi * S1_SEG;
   const int nseg = min(S1_SEG, Nt - y0);
   const int W = nseg + 2 * M - 1;  // window cell u <-> binning cell y0 - m + u
   // 1. virtual position of the first node of window cell u (u = W: one past the window's last node)
@@ -236,11 +249,7 @@ __global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T
     for (int i = 0; i < U; ++i) {
       v[i].x = (T)0;
       v[i].y = (T)0;
-#ifdef S1X_COALESCED_F
-      if (jj[i] >= 0) v[i] = fb[pp[i]];
-#else
       if (jj[i] >= 0) v[i] = fb[jj[i]];
-#endif
     }
 #pragma unroll
     for (int i = 0; i < U; ++i) {
@@ -254,12 +263,7 @@ __global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T
 #pragma unroll
         for (int l = 0; l < TAPS; ++l) w[l] = __ldg(wt + (long long)pp[i] * TAPS + l);
       } else {
-#ifdef S1X_NO_TAPS
-#pragma unroll
-        for (int l = 0; l < TAPS; ++l) w[l] = (T)frac;
-#else
         window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
-#endif
       }
       T* row = stap + q * TP;
 #pragma unroll
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T
       dst[sk] = acc[k];
     }
   }
+  }  // segments
 }
 
 // ---------------------------------------------------------------- TENSOR precompute (D = 1)

@@ -57,11 +57,18 @@ def _run(w, **kw):
 
 
 def _oracle(w, batches=None):
-    bs = range(w["batch"]) if batches is None else batches
+    bs = list(range(w["batch"])) if batches is None else list(batches)
     nodes = w["nodes"].astype(np.float64)
-    rf = np.stack([onfft.forward(nodes, w["fhat"][b].astype(np.complex128), w["N"], w["m"], w["sigma"]) for b in bs])
-    ry = np.stack([onfft.adjoint(nodes, w["f"][b].astype(np.complex128), w["N"], w["m"], w["sigma"]) for b in bs])
+    rf = onfft.forward(nodes, w["fhat"][bs].astype(np.complex128), w["N"], w["m"], w["sigma"])
+    ry = onfft.adjoint(nodes, w["f"][bs].astype(np.complex128), w["N"], w["m"], w["sigma"])
     return rf, ry
+
+
+def _check_features(w, **kw):
+    plan = _plan(w, **kw)
+    feats = plan.features()
+    plan.close()
+    return feats
 
 
 def _check(w, tol=None, **kw):
@@ -170,6 +177,27 @@ def test_2d_small_ragged_tiles(method, m):
     _check(w, method=method, tile=(20, 14))
 
 
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_2d_default_path_every_m(m):
+    """The default 2D kernels (interp_cell, warp-block spread_wb over the stored
+    taps) at every compiled m on a small ragged grid (config 3's m sweep is
+    3..8): default tiles and a ragged one."""
+    w = workloads.make("cfg3_2d_512", seed=11 + m, N=(48, 42), M=2500, m=m)
+    feats = _check_features(w)
+    assert "cell_mode" in feats and "wblock" in feats, feats
+    _check(w, tile=(20, 14))
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_3d_default_path_every_m(m):
+    """The default 3D kernels at every compiled m: interp_cell and the warp-block
+    adjoint (last dimension long enough for 8 + 2m - 1 cells), ragged tiles."""
+    w = workloads.make("cfg4_3d_64", seed=21 + m, N=(14, 12, 12), M=1500, m=m)
+    feats = _check_features(w)
+    assert "cell_mode" in feats and "wblock" in feats, feats
+    _check(w, tile=(6, 5, 7))
+
+
 @pytest.mark.parametrize("method", ["tiled", "tiled_cas", "tiled_loc", "tiled_sorted", "direct"])
 @pytest.mark.parametrize("m", [2, 4, 5])
 def test_3d_small_ragged_tiles(method, m):
@@ -199,25 +227,25 @@ def test_edge_cases_m1_node_one_cell_tiles_and_wrap():
     _check(w, method="direct")
 
 
-@pytest.mark.parametrize("config,ms", [("cfg2_1d_2e18", [3, 4, 8]), ("cfg3_2d_512", [3, 4, 8]), ("cfg4_3d_64", [4])])
-def test_full_size_configs(config, ms):
-    """BASELINE configs[1..3] at full size in the bench's launch configuration."""
-    for m in ms:
-        w = workloads.make(config, seed=0, m=m)
-        _check(w)
+@pytest.mark.parametrize("config,m", [("cfg2_1d_2e18", m) for m in range(3, 9)] +
+                         [("cfg3_2d_512", m) for m in range(3, 9)] + [("cfg4_3d_64", 4)])
+def test_full_size_configs(config, m):
+    """BASELINE configs[1..3] at full size in the bench's launch configuration,
+    every m of the sweep (m = 3..8 on the 1D / 2D sets)."""
+    w = workloads.make(config, seed=0, m=m)
+    _check(w)
 
 
 @pytest.mark.parametrize("config", ["cfg5_radial_s2", "cfg5_radial_s125"])
-def test_radial_batch_c64_sampled(config):
-    """BASELINE configs[4]: radial, B = 32, ComplexF32; the oracle checks three
-    of the 32 vectors (same launch as the bench: all 32 computed)."""
+def test_radial_batch_c64_all_vectors(config):
+    """BASELINE configs[4]: radial, B = 32, ComplexF32, in the bench's launch
+    configuration; every one of the 32 vectors against the (batched) oracle."""
     w = workloads.make(config, seed=0)
     got_f, got_y, _ = _run(w)
-    bs = [0, 17, 31]
-    rf, ry = _oracle(w, bs)
-    for i, b in enumerate(bs):
-        assert rel_l2(got_f[b], rf[i]) <= 2e-5
-        assert rel_l2(got_y[b], ry[i]) <= 2e-5
+    rf, ry = _oracle(w)
+    for b in range(w["batch"]):
+        assert rel_l2(got_f[b], rf[b]) <= 2e-5, b
+        assert rel_l2(got_y[b], ry[b]) <= 2e-5, b
 
 
 # ------------------------------------------------------------------ invariants / API paths
@@ -448,7 +476,8 @@ def test_one_kernel_sort_matches_three_kernel_sort(config):
     np.testing.assert_array_equal(oa, ob)
 
 
-@pytest.mark.parametrize("config", ["cfg1_1d_256", "cfg2_1d_2e18", "cfg3_2d_512", "cfg4_3d_64", "cfg5_radial_s2"])
+@pytest.mark.parametrize("config", ["cfg1_1d_256", "cfg2_1d_2e18", "cfg3_2d_512", "cfg4_3d_64", "cfg5_radial_s2",
+                                    "cfg5_radial_s125"])
 def test_cell_binning_bit_exact(config):
     """Cell mode: the hot-path sort is the oracle's binning with tile = 1 cell
     (key = row-major cell, ties by node index), bit-exact, including the radial
@@ -489,7 +518,8 @@ def test_1d_precompute_strategies(precompute, case):
     _check(w, precompute=precompute)
 
 
-@pytest.mark.parametrize("case", ["2d_c64_b32", "2d_c128_b9", "radial_b33_s125", "2d_c64_b8_m8"])
+@pytest.mark.parametrize("case", ["2d_c64_b32", "2d_c128_b9", "radial_b33_s125", "2d_c64_b8_m8"] +
+                         [f"2d_c128_b8_m{mm}" for mm in (1, 2, 5, 6, 7)] + [f"2d_c64_b16_m{mm}" for mm in (5, 6, 7)])
 def test_batch_adjoint(case):
     """2D batches of >= 8 transforms: row-segment adjoint with lanes = batch
     vectors (resample_rowbatch.cuh); every vector against the oracle, ragged
@@ -500,6 +530,12 @@ def test_batch_adjoint(case):
         w = workloads.make("cfg3_2d_512", seed=14, N=(48, 40), M=1500, m=3, batch=9)
     elif case == "2d_c64_b8_m8":
         w = workloads.make("cfg5_radial_s2", seed=17, N=(48, 64), M=900, m=8, batch=8)
+    elif case.startswith("2d_c128_b8_m"):
+        mm = int(case[-1])
+        w = workloads.make("cfg3_2d_512", seed=18 + mm, N=(48, 64), M=1000, m=mm, batch=8)
+    elif case.startswith("2d_c64_b16_m"):
+        mm = int(case[-1])
+        w = workloads.make("cfg5_radial_s2", seed=28 + mm, N=(40, 48), M=1100, m=mm, batch=16)
     else:
         w = workloads.make("cfg5_radial_s125", seed=16, N=(64, 64), M=2000, m=4, batch=33)
     plan = _plan(w)
@@ -671,16 +707,20 @@ def test_warp_block_adjoint(case):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("D", [2, 3])
-def test_warp_block_shards_and_fallback(D, monkeypatch):
-    """Node shards through the warp-block adjoint sum to the full adjoint; the
-    spread_cell fallback (NFFTB_NO_WB) agrees with it."""
+def test_warp_block_shards_and_fallback(D):
+    """Node shards through the warp-block adjoint sum to the full adjoint; on a
+    grid whose last dimension is too short for the warp blocks (Ntilde_last <
+    32 + 2m - 1 in 2D, 8 + 2m - 1 in 3D) the spread_cell fallback takes the
+    plan and matches the oracle."""
     torch = _torch()
     import paper_2208_00049_b200 as pkg
     from paper_2208_00049_b200 import dist
     if D == 2:
         w = workloads.make("cfg3_2d_512", seed=31, N=(32, 48), M=4000, m=4)
+        small = workloads.make("cfg3_2d_512", seed=33, N=(40, 12), M=2000, m=4)
     else:
         w = workloads.make("cfg4_3d_64", seed=32, N=(12, 12, 12), M=3000, m=3)
+        small = workloads.make("cfg4_3d_64", seed=34, N=(12, 10, 6), M=2000, m=3)
     _, full_y, _ = _run(w)
     _, ry = _oracle(w)
     assert rel_l2(full_y[0], ry[0]) <= TOL["c128"]
@@ -692,12 +732,24 @@ def test_warp_block_shards_and_fallback(D, monkeypatch):
         acc += plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
         plan.close()
     assert rel_l2(acc, full_y) < 1e-14
-    monkeypatch.setenv("NFFTB_NO_WB", "1")
-    plan = _plan(w)
-    assert "wblock" not in plan.features()
-    y_cell = plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
+    plan = _plan(small)
+    feats = plan.features()
     plan.close()
-    assert rel_l2(y_cell, full_y) < 1e-14
+    assert "wblock" not in feats and "cell_mode" in feats, feats
+    _check(small)
+
+
+@pytest.mark.gpu
+def test_large_tile_without_cell_adjoint_drops_to_direct():
+    """A tile beyond the spread_cell fallback's limits (> 512 gather items) on a
+    grid too short for the warp blocks: no cell-mode adjoint exists, so the
+    plan leaves cell mode (unblocked kernels) and still matches the oracle."""
+    w = workloads.make("cfg3_2d_512", seed=35, N=(128, 12), M=2500, m=4)
+    plan = _plan(w, tile=(128, 24))
+    feats = plan.features()
+    plan.close()
+    assert "cell_mode" not in feats, feats
+    _check(w, tile=(128, 24))
 
 
 @pytest.mark.gpu

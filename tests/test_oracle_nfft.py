@@ -262,3 +262,19 @@ def test_window_2m_plus_2_adjoint_identity():
     AHf = nfft.adjoint(nodes, f, (24, 20), 3, 2.0, window_points="2m+2")
     lhs, rhs = np.vdot(f, Af), np.vdot(AHf, fhat)
     assert abs(lhs - rhs) / (np.linalg.norm(Af) * np.linalg.norm(f)) < 1e-14
+
+
+def test_batched_oracle_equals_per_vector_calls():
+    """The batched forms of resample_forward / resample_adjoint (footprints and
+    taps evaluated once for B vectors on the same nodes) give exactly the
+    per-vector results: the per-vector arithmetic is the same sequence of
+    operations (PAPER.md:482-483 applied to each vector)."""
+    w = workloads.make("cfg5_radial_s2", seed=3, N=(20, 16), M=300, m=3, batch=4)
+    nodes = w["nodes"].astype(np.float64)
+    fhat = w["fhat"].astype(np.complex128)
+    f = w["f"].astype(np.complex128)
+    fb = nfft.forward(nodes, fhat, w["N"], 3, 2.0)
+    yb = nfft.adjoint(nodes, f, w["N"], 3, 2.0)
+    for b in range(4):
+        np.testing.assert_array_equal(fb[b], nfft.forward(nodes, fhat[b], w["N"], 3, 2.0))
+        np.testing.assert_array_equal(yb[b], nfft.adjoint(nodes, f[b], w["N"], 3, 2.0))

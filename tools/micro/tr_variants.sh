@@ -4,5 +4,5 @@ out=$1; shift
 mkdir -p $out
 for v in "$@"; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -I include $v -o /tmp/trace1d tools/micro/trace1d.cu || continue
-  for mode in flushed warm; do echo "== $v $mode" >> $out/tr.json; /tmp/trace1d 4 $mode | head -2 >> $out/tr.json; done
+  for mode in flushed warm; do echo "== $v $mode S1CAP=$S1CAP" >> $out/tr.json; /tmp/trace1d 4 $mode | head -3 >> $out/tr.json; done
 done

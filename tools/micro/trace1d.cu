@@ -26,7 +26,13 @@ __global__ void __launch_bounds__(128) empty_kernel(Geom g, WinPoly<T> wp, doubl
 __global__ void __launch_bounds__(128) empty_small(double2* out, int n) {
   if (threadIdx.x == 0 && blockIdx.x == 100000) out[0] = make_double2(n, n);
 }
-static bool g_flush = true;  // L2 flush before every launch (argv[2] = "warm": no flush)
+__global__ void permute_scatter(const double2* __restrict__ f, const int* __restrict__ inv, double2* __restrict__ fc,
+                                int M) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < M) fc[inv[j]] = f[j];
+}
+static bool g_flush = true;
+static unsigned g_s1cap = 0;  // spread1s CTAs per SM (0: one per segment); env S1CAP  // L2 flush before every launch (argv[2] = "warm": no flush)
 
 template <int M>
 static void run(int M_nodes, int Nt) {
@@ -85,7 +91,7 @@ static void run(int M_nodes, int Nt) {
   const size_t sb = s1_smem_bytes(M, 16, 8), ib = i1_smem_bytes(M, 16);
   cudaFuncSetAttribute((const void*)spread1s_kernel<double, M, DEG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
   cudaFuncSetAttribute((const void*)interp1s_kernel<double, M, DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib);
-  const unsigned segs_s = (Nt + S1_SEG - 1) / S1_SEG, segs_i = (Nt + I1_SEG - 1) / I1_SEG;
+  const unsigned segs_s = std::min<unsigned>((Nt + S1_SEG - 1) / S1_SEG, g_s1cap ? g_s1cap * 148 : 1u << 30), segs_i = (Nt + I1_SEG - 1) / I1_SEG;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -113,6 +119,14 @@ static void run(int M_nodes, int Nt) {
     const float te = b2b([&] { empty_kernel<double><<<1024, 128, 0, st>>>(g, wpbig, d_out); });
     const float tes = b2b([&] { empty_small<<<1024, 128, 0, st>>>(d_out, 1); });
     const float tes1 = b2b([&] { empty_small<<<1, 32, 0, st>>>(d_out, 1); });
+    int* d_inv;
+    cudaMalloc(&d_inv, M_nodes * 4);
+    {
+      std::vector<int> inv(M_nodes);
+      for (int p = 0; p < M_nodes; ++p) inv[jc[p]] = p;
+      cudaMemcpy(d_inv, inv.data(), M_nodes * 4, cudaMemcpyHostToDevice);
+    }
+    const float tperm = b2b([&] { permute_scatter<<<(M_nodes + 255) / 256, 256, 0, st>>>(d_f, d_inv, d_out, M_nodes); });
     cudaGraph_t gr;
     cudaGraphExec_t ge;
     cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
@@ -123,7 +137,7 @@ static void run(int M_nodes, int Nt) {
     cudaGraphInstantiate(&ge, gr, 0);
     const float tg = b2b([&] { cudaGraphLaunch(ge, st); }) / 20;
     printf("{\"b2b_us\": {\"spread1s\": %.2f, \"interp1s\": %.2f, \"spread1s_graph\": %.2f, \"empty_1024x128_bigparams\": %.2f, "
-           "\"empty_1024x128\": %.2f, \"empty_1x32\": %.2f}}\n", ts, ti, tg, te, tes, tes1);
+           "\"empty_1024x128\": %.2f, \"empty_1x32\": %.2f, \"permute_scatter\": %.2f}}\n", ts, ti, tg, te, tes, tes1, tperm);
   }
   for (int which = 0; which < 2; ++which) {
     const unsigned nctas = which == 0 ? segs_s : segs_i;
@@ -179,6 +193,7 @@ static void run(int M_nodes, int Nt) {
 int main(int argc, char** argv) {
   const int m = argc > 1 ? atoi(argv[1]) : 4;
   if (argc > 2 && std::string(argv[2]) == "warm") g_flush = false;
+  if (getenv("S1CAP")) g_s1cap = atoi(getenv("S1CAP"));
   if (m == 8) run<8>(1 << 18, 1 << 19);
   else run<4>(1 << 18, 1 << 19);
   printf("{\"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
