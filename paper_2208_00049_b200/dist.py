@@ -32,10 +32,19 @@ def shard_range(n, rank, world):
     return begin, end
 
 
+SELF = "self"  # a group of this rank alone (no node sharding; distinct from None = the world)
+
+
 def _world(group):
-    if not dist.is_available() or not dist.is_initialized():
+    if group is SELF or not dist.is_available() or not dist.is_initialized():
         return 1
     return dist.get_world_size(group)
+
+
+def _rank(group):
+    if group is SELF or not dist.is_available() or not dist.is_initialized():
+        return 0
+    return dist.get_rank(group)
 
 
 def allreduce_sum(t, group=None):
@@ -60,8 +69,7 @@ class ShardedNfft:
     def __init__(self, nodes, N, group=None, **plan_kw):
         from . import NfftPlan
         self.group = group
-        init = dist.is_available() and dist.is_initialized()
-        self.rank = dist.get_rank(group) if init else 0
+        self.rank = _rank(group)
         self.world = _world(group)
         M = int(nodes.shape[0])
         self.range = shard_range(M, self.rank, self.world)
@@ -94,13 +102,13 @@ def grid_groups(world, g_n):
     """Rank layout of a G_b x G_n grid: rank r is in batch group r // g_n and
     node-shard position r % g_n. Returns (batch_group_index, n_batch_groups,
     node_group) where node_group is the process group of the g_n ranks sharing
-    this rank's batch slice (None when g_n == 1). Every rank must call this
+    this rank's batch slice (SELF when g_n == 1). Every rank must call this
     (new_group is collective)."""
     if g_n < 1 or world % g_n:
         raise ValueError(f"node-shard group size {g_n} must divide the world size {world}")
     rank = dist.get_rank() if dist.is_initialized() else 0
     n_b = world // g_n
-    mine = None
+    mine = SELF
     if g_n > 1:
         for gb in range(n_b):
             grp = dist.new_group(list(range(gb * g_n, (gb + 1) * g_n)))

@@ -77,3 +77,34 @@ def test_two_rank_gloo_shards_sum_to_full_transform(tmp_path):
     ref_y = onfft.adjoint(w["nodes"], w["f"][0], w["N"], 3, 2.0)
     assert rel_l2(np.load(tmp_path / "f.npy"), ref_f) < 1e-14
     assert rel_l2(np.load(tmp_path / "y.npy"), ref_y) < 1e-14
+
+
+def _grid_worker(rank, world, port, out_dir, g_n):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2208_00049_b200.dist import allreduce_sum, grid_groups, shard_range
+    gb, n_b, grp = grid_groups(world, g_n)
+    b0, b1 = shard_range(32, gb, n_b)
+    # the node group sums ones: its size
+    t = torch.ones(1)
+    allreduce_sum(t, grp)
+    np.save(os.path.join(out_dir, f"r{rank}.npy"), np.array([gb, n_b, b0, b1, int(t.item())]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("g_n", [1, 2, 4])
+def test_four_rank_batch_by_node_grid(g_n, tmp_path):
+    """HybridNfft's rank layout (dist.grid_groups): G = 4 ranks as G_b x G_n;
+    the batch groups partition the 32 vectors of config 5, and the node-shard
+    group of every rank has G_n members."""
+    mp.spawn(_grid_worker, args=(4, _free_port(), str(tmp_path), g_n), nprocs=4, join=True)
+    rows = [np.load(tmp_path / f"r{r}.npy") for r in range(4)]
+    seen = {}
+    for r, (gb, n_b, b0, b1, size) in enumerate(rows):
+        assert gb == r // g_n and n_b == 4 // g_n and size == g_n
+        seen[gb] = (b0, b1)
+    spans = sorted(seen.values())
+    assert spans[0][0] == 0 and spans[-1][1] == 32
+    assert all(e0 == b1 for (_, e0), (b1, _) in zip(spans[:-1], spans[1:]))
