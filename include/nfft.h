@@ -17,9 +17,10 @@
  *    NFFT_COMPLEX128), coordinate d fastest. Nominally in [-1/2, 1/2)^D
  *    (PAPER.md:90); any finite value is folded periodically.
  *  - N-grid arrays: C-contiguous (B, N_0, ..., N_{D-1}) interleaved complex
- *    (re, im) of the plan precision; storage index i_d <-> n_d = i_d - N_d/2,
- *    n_d in [-N_d/2, N_d/2). Node coordinate d pairs with
- *    grid axis d; the last axis is contiguous.
+ *    (re, im) of the plan precision; storage index i_d <-> n_d = i_d - floor(N_d/2),
+ *    n_d in [-N_d/2, N_d/2) for even N_d and [-(N_d-1)/2, (N_d-1)/2] for odd
+ *    N_d. Node coordinate d pairs with grid axis d; the last
+ *    axis is contiguous.
  *  - node-value arrays: (B, M) interleaved complex, caller's node order.
  *  - Pointers to data may be device pointers or host pointers (pageable or
  *    pinned); host data is staged through plan-owned device buffers on the
@@ -53,7 +54,7 @@ typedef enum { NFFT_COMPLEX64 = 0, NFFT_COMPLEX128 = 1 } nfft_precision;
 typedef enum {
   NFFT_SUCCESS = 0,
   NFFT_ERROR_INVALID_VALUE = 1,   /* null pointer, D not in 1..3, M < 1, m < 1, B < 1, unknown enum */
-  NFFT_ERROR_BAD_GEOMETRY = 2,    /* odd or < 2 N_d, sigma <= 1, 2m >= Ntilde_d */
+  NFFT_ERROR_BAD_GEOMETRY = 2,    /* N_d < 2, sigma <= 1, 2m >= Ntilde_d */
   NFFT_ERROR_NONFINITE_NODE = 3,  /* a node coordinate is NaN/Inf (reported by nfft_precompute) */
   NFFT_ERROR_BAD_TILE = 4,        /* tile_d < 0, tile_d > Ntilde_d, or tile+halo exceeds shared memory */
   NFFT_ERROR_NOT_PRECOMPUTED = 5, /* forward/adjoint before nfft_precompute */

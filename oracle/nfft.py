@@ -26,8 +26,10 @@ def geometry(N, sigma, m, window_points="2m"):
     """Plan geometry (readings R3/R4).
 
     Ntilde_d = 2 ceil(sigma N_d / 2); beta_d = pi m (2 - N_d / Ntilde_d).
-    Raises ValueError on the invalid geometries DESIGN.md lists (odd N_d,
-    sigma <= 1, 2m >= Ntilde_d; 2m+2 >= Ntilde_d for the 2m+2 variant).
+    Raises ValueError on the invalid geometries DESIGN.md lists (N_d < 2,
+    sigma <= 1, 2m >= Ntilde_d; 2m+2 >= Ntilde_d for the 2m+2 variant). Odd
+    N_d are valid: I_N then covers n_d = -(N_d-1)/2 .. (N_d-1)/2,
+    storage index i_d = n_d + floor(N_d/2) (reading R18).
     window_points: "2m" (the paper's truncated psi_hat) or
     "2m+2" (NFFT3's variant: 2m+2 samples of the continued
     window, same shape beta and correction).
@@ -41,8 +43,8 @@ def geometry(N, sigma, m, window_points="2m"):
         raise ValueError("m must be >= 1")
     Ntilde = []
     for n in N:
-        if n < 2 or n % 2:
-            raise ValueError("N_d must be even and >= 2")
+        if n < 2:
+            raise ValueError("N_d must be >= 2")
         Ntilde.append(2 * math.ceil(sigma * n / 2.0))
     npts = 2 * m if window_points == "2m" else 2 * m + 2
     for nt in Ntilde:
@@ -53,7 +55,8 @@ def geometry(N, sigma, m, window_points="2m"):
 
 
 def _logical_axes(N):
-    """n_d in I_{N_d} = [-N_d/2, N_d/2) in storage order."""
+    """n_d in I_{N_d} = Z cap [-N_d/2, N_d/2) in storage order:
+    -N_d/2 .. N_d/2-1 for even N_d, -(N_d-1)/2 .. (N_d-1)/2 for odd N_d."""
     return [np.arange(-(n // 2), n - n // 2, dtype=np.int64) for n in N]
 
 

@@ -1002,7 +1002,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   int64_t Nt[3] = {1, 1, 1};
   int64_t cells = 1, ncells = 1;
   for (int d = 0; d < D; ++d) {
-    if (N[d] < 2 || (N[d] & 1)) return NFFT_ERROR_BAD_GEOMETRY;
+    if (N[d] < 2) return NFFT_ERROR_BAD_GEOMETRY;  // odd N_d: n_d = -(N_d-1)/2 .. (N_d-1)/2
     if (N[d] > (int64_t)1 << 30) return NFFT_ERROR_UNSUPPORTED;
     Nt[d] = 2 * (int64_t)std::ceil(sigma * (double)N[d] / 2.0);
     if (2 * (int64_t)m >= Nt[d]) return NFFT_ERROR_BAD_GEOMETRY;
@@ -1467,7 +1467,7 @@ const char* nfft_status_string(nfft_status s) {
   switch (s) {
     case NFFT_SUCCESS: return "success";
     case NFFT_ERROR_INVALID_VALUE: return "invalid value";
-    case NFFT_ERROR_BAD_GEOMETRY: return "bad geometry (N_d even >= 2, sigma > 1, 2m < Ntilde_d)";
+    case NFFT_ERROR_BAD_GEOMETRY: return "bad geometry (N_d >= 2, sigma > 1, 2m < Ntilde_d)";
     case NFFT_ERROR_NONFINITE_NODE: return "non-finite node coordinate";
     case NFFT_ERROR_BAD_TILE: return "bad tile size";
     case NFFT_ERROR_NOT_PRECOMPUTED: return "plan not precomputed";

@@ -71,9 +71,9 @@ def test_argument_validation_before_any_device_work(libpath):
     assert create(ctypes.byref(h), 1, N, 2, nodes, 2.0, 9, 0, 1) == 9   # m > 8
     N8 = (ctypes.c_int64 * 1)(8)
     assert create(ctypes.byref(h), 1, N8, 2, nodes, 2.0, 8, 0, 1) == 2  # 2m = 16 >= Ntilde = 16
-    # odd N
-    Nodd = (ctypes.c_int64 * 1)(15)
-    assert create(ctypes.byref(h), 1, Nodd, 2, nodes, 2.0, 2, 0, 1) == 2
+    # N_d < 2 (odd N_d >= 3 are valid: PAPER.md:89)
+    N1 = (ctypes.c_int64 * 1)(1)
+    assert create(ctypes.byref(h), 1, N1, 2, nodes, 2.0, 2, 0, 1) == 2
     assert create(ctypes.byref(h), 1, N, 2, nodes, 2.0, 2, 5, 1) == 1   # unknown window
     # batch outside [1, 65535] (nfft_options.batch)
     opt = pkg.Options()

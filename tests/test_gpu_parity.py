@@ -768,3 +768,27 @@ def test_large_tiles_keep_cell_mode(case):
     plan.close()
     assert "cell_mode" in feats and feat in feats, feats
     _check(w, tile=tile)
+
+
+@pytest.mark.parametrize("case", ["1d_c128", "1d_c64_m7", "2d_mixed_c128", "2d_odd_batch9_c64", "3d_odd_c128",
+                                  "2d_odd_direct"])
+def test_odd_n(case):
+    """Odd N_d (n_d = -(N_d-1)/2 .. (N_d-1)/2, storage i = n + (N_d-1)/2)
+    through the default kernels (and the unblocked ones) against the oracle."""
+    kw = {}
+    if case == "1d_c128":
+        w = workloads.make("cfg2_1d_2e18", seed=61, N=(1001,), M=900, m=4)
+    elif case == "1d_c64_m7":
+        w = workloads.make("cfg2_1d_2e18", seed=62, N=(333,), M=500, m=7)
+        w = dict(w, nodes=w["nodes"].astype(np.float32), fhat=w["fhat"].astype(np.complex64),
+                 f=w["f"].astype(np.complex64), precision="c64")
+    elif case == "2d_mixed_c128":
+        w = workloads.make("cfg3_2d_512", seed=63, N=(45, 52), M=2500, m=5)
+    elif case == "2d_odd_batch9_c64":
+        w = workloads.make("cfg5_radial_s125", seed=64, N=(63, 61), M=1500, m=4, batch=9)
+    elif case == "3d_odd_c128":
+        w = workloads.make("cfg4_3d_64", seed=65, N=(13, 11, 15), M=1500, m=3)
+    else:
+        w = workloads.make("cfg3_2d_512", seed=66, N=(23, 31), M=800, m=4)
+        kw = dict(method="direct")
+    _check(w, **kw)

@@ -201,9 +201,52 @@ def test_footprint_golden_examples():
 
 def test_geometry_validation():
     assert nfft.geometry((256, 100), 1.25, 4)["Ntilde"] == (320, 126)
-    for bad in [((7,), 2.0, 2), ((8,), 1.0, 2), ((8,), 2.0, 8)]:
+    # odd N_d are valid; Ntilde_d = 2 ceil(sigma N_d / 2) stays even
+    assert nfft.geometry((15, 9), 2.0, 3)["Ntilde"] == (30, 18)
+    assert nfft.geometry((9,), 1.25, 2)["Ntilde"] == (12,)
+    for bad in [((1,), 2.0, 1), ((8,), 1.0, 2), ((8,), 2.0, 8)]:
         with pytest.raises(ValueError):
             nfft.geometry(*bad)
+
+
+# ------------------------------------------------------- odd N
+
+def test_odd_n_index_set_and_equispaced_ndft():
+    """Odd N: I_N = {-(N-1)/2, ..., (N-1)/2}, storage i = n + (N-1)/2.
+    With k_j = j/N - 1/2 the NDFT is a DFT:
+    fhat_j = e^{2 pi i h j/N} FFT(f_i (-1)^(i-h))_j, h = (N-1)/2 (library FFT)."""
+    for N in (15, 33):
+        h = (N - 1) // 2
+        rng = np.random.default_rng(N)
+        f = workloads.complex_normal(rng, (N,))
+        nodes = (np.arange(N) / N - 0.5)[:, None]
+        i = np.arange(N)
+        ref = np.exp(2j * np.pi * h * i / N) * np.fft.fft(f * (-1.0) ** (i - h))
+        assert rel_inf(ndft.ndft(nodes, f, (N,)), ref) < 1e-13
+        assert rel_inf(ndft.adjoint_ndft(nodes, ndft.ndft(nodes, f, (N,)), (N,)) / N, f) < 1e-13
+
+
+@pytest.mark.parametrize("N,M,m", [((15,), 60, 6), ((9, 12), 150, 5), ((5, 7, 6), 120, 4)])
+def test_odd_n_nfft_matches_ndft(N, M, m):
+    """Odd N in 1D, 2D (mixed odd/even), 3D: the NFFT (Alg. 1 / 2) against the
+    brute-force NDFT; the error is the window's (sigma = 2: ~ 90x smaller per m)."""
+    nodes, fhat, f = _rand(40 + len(N), M, N)
+    ef = rel_l2(nfft.forward(nodes, fhat, N, m, 2.0), ndft.ndft(nodes, fhat, N))
+    ey = rel_l2(nfft.adjoint(nodes, f, N, m, 2.0), ndft.adjoint_ndft(nodes, f, N))
+    bound = {4: 3e-7, 5: 3e-9, 6: 3e-11}[m]
+    assert ef < bound and ey < bound, (ef, ey)
+
+
+def test_odd_n_delta_and_single_node():
+    """Odd N: delta at n = 0 (storage (N-1)/2) gives fhat_j = 1; one node at k = 0
+    with value 1 gives y_n = 1 for every n in I_N (eq. NDFT / NDFTH)."""
+    N = 21
+    nodes = (np.arange(N) / N - 0.5)[:, None]
+    fh = np.zeros(N, complex)
+    fh[(N - 1) // 2] = 1.0
+    assert np.max(np.abs(nfft.forward(nodes, fh, (N,), 8, 2.0) - 1.0)) < 1e-13
+    y = nfft.adjoint(np.zeros((1, 2)), np.array([1.0 + 0j]), (17, 15), 7, 2.0)
+    assert y.shape == (17, 15) and np.max(np.abs(y - 1.0)) < 5e-12  # the window error at m = 7
 
 
 @pytest.mark.slow
