@@ -66,6 +66,7 @@ def parse(argv=None):
     ap.add_argument("--tile", default="")
     ap.add_argument("--no-sweep", action="store_true", help="skip the m = 3..8 sweep")
     ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs")
+    ap.add_argument("--no-strategies", action="store_true", help="skip the precompute-strategy table")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline measurement")
     ap.add_argument("--no-graph", action="store_true", help="launch the step kernel by kernel (no CUDA graph)")
@@ -621,6 +622,47 @@ def measure_e2e(a, ctx, w, steps=None):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps}
 
 
+def measure_strategies(a, ctx, steps=20, warmup=3):
+    """The window precomputation strategies (the paper's Fig. 4
+    compares their transform time and precomputation time):
+    per config and strategy, the step throughput (direct + adjoint, as the main
+    line) and the precompute time (nfft_precompute alone, L2 flushed, graph)."""
+    import torch
+    import argparse as _ap
+    out = {}
+    for config in ("cfg2_1d_2e18",) + OTHER_CONFIGS:
+        w = make_workload(a, ctx, config, "weak", None)
+        D, M, m = len(w["N"]), w["M"], w["m"]
+        r = 8 if w["precision"] == "c128" else 4
+        table = {"polynomial": 0, "tensor": M * D * 2 * m * r, "full": M * (2 * m) ** D * (r + 4)}
+        out[config] = {}
+        for strat in ("polynomial", "tensor", "full"):
+            aa = _ap.Namespace(**vars(a))
+            aa.precompute = strat
+            res = run_steps(aa, ctx, w, "weak", steps, warmup)
+            obj, plan, *_ = build(aa, ctx, w, "weak")
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=ctx.stream):
+                plan.run_stage("precompute")
+            times = []
+            for _ in range(10):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(ctx.stream):
+                    flush(ctx)
+                    e0.record(ctx.stream)
+                    g.replay()
+                    e1.record(ctx.stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+            feats = sorted(plan.features())
+            del g
+            obj.close()
+            out[config][strat] = {"value": res["units_total"] * steps / (res["ms"] * 1e-3), "unit": UNIT,
+                                  "ms_per_step": res["ms"] / steps, "precompute_ms": statistics.median(times),
+                                  "table_bytes": table[strat], "features": feats}
+    return out
+
+
 def relaunch(a):
     """`bench.py --gpus N` without torchrun: launch N ranks (one per GPU) with
     torch.distributed.run on 127.0.0.1 and return their exit code."""
@@ -676,6 +718,10 @@ def main():
                                       "spread_ms": r["stages_ms_marginal"]["spread"], "roofline_frac": r["roofline"]["frac"],
                                       "roofline_bound": r["roofline"]["bound"]}
 
+    strategies = None
+    if not a.no_strategies and ctx.world == 1:
+        strategies = measure_strategies(a, ctx)
+
     if ctx.rank == 0:
         line = {
             "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": ctx.world, "steps": a.steps,
@@ -693,6 +739,8 @@ def main():
             line["configs"] = configs
         if sweep:
             line["m_sweep"] = sweep
+        if strategies:
+            line["strategies"] = strategies
         print(json.dumps(line), flush=True)
     if ctx.world > 1:
         import torch.distributed as dist

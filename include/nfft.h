@@ -81,15 +81,19 @@ typedef enum {
                               static-tile interp / owner-computes spread when Q | Ntilde, P >= 3, Q >= 2m) */
 } nfft_method;
 
-/* Window precomputation strategy (Fig. 4 at PAPER.md:748-765). */
+/* Window precomputation strategy (Fig. 4 at PAPER.md:748-765). Cell mode only
+ * (methods AUTO / TILED); plans that fall back to the unblocked kernels use POLYNOMIAL. */
 typedef enum {
-  NFFT_PRECOMPUTE_AUTO = 0,       /* POLYNOMIAL (measured faster on B200 at every config); the
-                                     D = 2, 3 adjoints store the taps regardless (precompute table) */
-  NFFT_PRECOMPUTE_POLYNOMIAL = 1, /* taps evaluated per call from the piecewise polynomial */
-  NFFT_PRECOMPUTE_TENSOR = 2      /* the 2m D taps of every node stored by nfft_precompute (PAPER.md:599-604,
-                                     "TENSOR": 2m D M reals; trades FP work for memory traffic);
-                                     implemented for the D = 1 cell-mode adjoint (thread per cell
-                                     gather over the stored taps), ignored elsewhere */
+  NFFT_PRECOMPUTE_AUTO = 0,       /* POLYNOMIAL (measured fastest on B200) */
+  NFFT_PRECOMPUTE_POLYNOMIAL = 1, /* taps evaluated per call from the piecewise polynomial;
+                                     the D = 2, 3 warp-block / batch adjoints still read a tap table that
+                                     nfft_precompute builds */
+  NFFT_PRECOMPUTE_TENSOR = 2,     /* "TENSOR": the 2m taps per dimension of every node
+                                     (2m D M reals) stored by nfft_precompute; every resampling kernel reads them */
+  NFFT_PRECOMPUTE_FULL = 3        /* "FULL" (CuNFFT PAPER.md:800): the sparse matrix B
+                                     itself, (2m)^D weights + int32 grid indices per node (E (r + 4) M bytes,
+                                     PAPER.md:646-659); forward = sparse matrix-vector product, adjoint =
+                                     owner-computes gather over the stored weights */
 } nfft_precompute_strategy;
 
 typedef struct {
@@ -105,8 +109,7 @@ typedef struct {
   int check_nodes;        /* 1 (default): nfft_precompute synchronises once and reports
                              NFFT_ERROR_NONFINITE_NODE; 0: fully asynchronous, no check
                              (non-finite nodes then give unspecified values, never a fault) */
-  int precompute;         /* nfft_precompute_strategy (default AUTO); TENSOR is used where a kernel
-                             for it exists (D = 1, cell mode) and is ignored elsewhere */
+  int precompute;         /* nfft_precompute_strategy (default AUTO) */
   int window_points;      /* 0 (default): 2m samples of the truncated window psi_hat;
                              1: NFFT3's 2m+2 samples of the analytically continued window, same
                              shape beta and correction; needs m <= 7 and 2m+2 < Ntilde_d */
@@ -244,11 +247,13 @@ nfft_status nfft_autotune_tile(int D, const int64_t* N, int64_t M, const void* n
  *   NFFT_FEATURE_CELL_MODE   nodes sorted by cell, cell-mode resampling kernels
  *   NFFT_FEATURE_TENSOR      TENSOR precompute (stored taps)
  *   NFFT_FEATURE_BATCH       2D batch adjoint: row segments, lanes = batch vectors (B >= 8)
- *   NFFT_FEATURE_WBLOCK      D = 2, 3 adjoint over warp-owned cell blocks and stored taps */
+ *   NFFT_FEATURE_WBLOCK      D = 2, 3 adjoint over warp-owned cell blocks and stored taps
+ *   NFFT_FEATURE_FULL        FULL precompute (the sparse matrix B stored) */
 #define NFFT_FEATURE_CELL_MODE 1
 #define NFFT_FEATURE_TENSOR 4
 #define NFFT_FEATURE_BATCH 8
 #define NFFT_FEATURE_WBLOCK 16
+#define NFFT_FEATURE_FULL 32
 nfft_status nfft_get_features(nfft_plan p, int* features);
 
 #ifdef __cplusplus

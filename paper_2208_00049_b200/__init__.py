@@ -29,7 +29,7 @@ NFFT_SYMBOLS = (
     "nfft_get_launch_count", "nfft_run_stage", "nfft_execute", "nfft_get_cell_binning", "nfft_get_features",
     "nfft_autotune_tile",
 )
-PRECOMPUTE = {"auto": 0, "polynomial": 1, "tensor": 2}
+PRECOMPUTE = {"auto": 0, "polynomial": 1, "tensor": 2, "full": 3}
 STAGES = {"precompute": 0, "fwd_deconv": 1, "fwd_fft": 2, "fwd_interp": 3, "adj_spread": 4, "adj_fft": 5,
           "adj_crop": 6}
 
@@ -128,8 +128,8 @@ class NfftPlan:
     -> torch CUDA out; numpy in -> numpy out (host staging inside the library).
     node_range: (begin, end) shard of the plan's SORTED node order (cell order
     in cell mode) processed by forward/adjoint (multi-GPU sharding, DESIGN.md
-    §Multi-GPU). precompute: "auto" | "polynomial" | "tensor" (window taps per
-    call vs stored by nfft_precompute). window_points: "2m" |
+    §Multi-GPU). precompute: "auto" | "polynomial" | "tensor" | "full" (window
+    taps per call / stored taps / the stored sparse matrix B). window_points: "2m" |
     "2m+2" (NFFT3's continued-window variant).
     """
 
@@ -359,10 +359,11 @@ class NfftPlan:
         return dict(deconv=ms[0], fft=ms[1], resample=ms[2], zero=ms[3], precompute=ms[4])
 
     def features(self):
-        """Paths in use: {"cell_mode", "tensor", "batch", "wblock"} (include/nfft.h: nfft_get_features)."""
+        """Paths in use: {"cell_mode", "tensor", "batch", "wblock", "full"} (include/nfft.h: nfft_get_features)."""
         v = ctypes.c_int()
         _check(lib().nfft_get_features(self._h, ctypes.byref(v)), "nfft_get_features")
-        return {k for k, bit in (("cell_mode", 1), ("tensor", 4), ("batch", 8), ("wblock", 16)) if v.value & bit}
+        return {k for k, bit in (("cell_mode", 1), ("tensor", 4), ("batch", 8), ("wblock", 16), ("full", 32))
+                if v.value & bit}
 
     def launches(self):
         n = ctypes.c_int64()

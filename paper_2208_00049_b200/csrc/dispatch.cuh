@@ -21,6 +21,7 @@ struct KernelSet {
   void (*spread_gather)(Geom, WinPoly<T>, const C*, const T*, const int*, const int4*, const int*, int, C*);
   // D = 1 static-tile kernels (resample1d.cuh)
   const void* interp1;  // takes WinPolyN<T, D, m> (launched with launch_k)
+  const void* interp1t;  // TENSOR: taps from the stored table
   const void* spread1;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 1 TENSOR precompute (taps stored by nfft_precompute) and the adjoint over them
   const void* taps1;  // takes WinPolyN<T, D, m> (launched with launch_k)
@@ -29,6 +30,11 @@ struct KernelSet {
   void (*interp_nd)(Geom, WinPoly<T>, const C*, const T*, const int*, const int*, int, int, C*);
   // D = 2, 3 over cell-sorted nodes (resample_cell.cuh)
   const void* interp_cell;  // takes WinPolyN<T, D, m> (launched with launch_k)
+  const void* interp_cellt;  // TENSOR: taps from the stored table
+  // FULL precompute strategy (resample_full.cuh): the sparse matrix B
+  const void* full_build;
+  const void* full_interp;
+  const void* full_spread;  // D >= 2
   const void* spread_cell;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 2 batches: row-segment spread, lanes = batch vectors (resample_rowbatch.cuh)
   void (*spread_rowbatch)(Geom, const C*, int, const T*, const int*, C*);
@@ -58,6 +64,7 @@ inline KernelSet<T> kernels_for(int D, int m) {
 #include "resample_cell.cuh"
 #include "resample_rowbatch.cuh"
 #include "resample_wblock.cuh"
+#include "resample_full.cuh"
 namespace nfftb {
 template <typename T, int D, int M>
 KernelSet<T> make_set() {
@@ -79,13 +86,18 @@ KernelSet<T> make_set() {
     k.spread_gather = spread_gather_kernel<T, D, M, DEG>;
   }
 #endif
+  k.full_build = (const void*)full_build_kernel<T, D, M, DEG>;
+  k.full_interp = (const void*)full_interp_kernel<T, D, M>;
   if constexpr (D == 1) {
-    k.interp1 = (const void*)interp1s_kernel<T, M, DEG>;
+    k.interp1 = (const void*)interp1s_kernel<T, M, DEG, false>;
+    k.interp1t = (const void*)interp1s_kernel<T, M, DEG, true>;
     k.spread1 = (const void*)spread1s_kernel<T, M, DEG, false>;
     k.taps1 = (const void*)taps1_kernel<T, M, DEG>;
     k.spread1t = (const void*)spread1s_kernel<T, M, DEG, true>;
   } else {
-    k.interp_cell = (const void*)interp_cell_kernel<T, D, M, DEG>;
+    k.interp_cell = (const void*)interp_cell_kernel<T, D, M, DEG, false>;
+    k.interp_cellt = (const void*)interp_cell_kernel<T, D, M, DEG, true>;
+    k.full_spread = (const void*)full_spread_kernel<T, D, M>;
     k.spread_cell = (const void*)spread_cell_kernel<T, D, M, DEG>;
     if constexpr (D == 2) k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
     k.taps_nd = (const void*)taps_nd_kernel<T, D, M, DEG>;

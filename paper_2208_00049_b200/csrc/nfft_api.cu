@@ -28,6 +28,7 @@
 #include "resample_cell.cuh"
 #include "resample_rowbatch.cuh"
 #include "resample_wblock.cuh"
+#include "resample_full.cuh"
 
 using namespace nfftb;
 
@@ -96,7 +97,11 @@ struct nfft_plan_s {
   size_t sc_bytes = 0;       // spread_cell shared memory
   int sc_cap = 0;            // spread_cell node slots per chunk
   void* d_kc = nullptr;      // D*M reals: coordinates in cell order (SoA)
-  bool tensor = false;       // TENSOR precompute (D = 1 cell mode): taps stored in cell order
+  bool tensor = false;       // TENSOR precompute (cell mode): the 2m D taps of every node stored in cell order
+  bool full = false;         // FULL precompute (cell mode): the rows of the sparse matrix B stored in cell order
+  int full_e = 0;            // entries per row, (2m)^D
+  void* d_bw = nullptr;      // FULL: M * E weights (plan precision)
+  int* d_bi = nullptr;       // FULL: M * E grid indices
   bool batchmode = false;    // D = 2 cell mode, B >= 8: row-segment spread with lanes = batch vectors
   int bp = 0;                // batch padded to a multiple of 32
   void* d_fT = nullptr;      // M * bp complex: node values, transposed (node-major)
@@ -190,7 +195,8 @@ void free_all(nfft_plan p) {
   void* bufs[] = {p->d_nodes, p->d_ks, p->d_offsets, p->d_subbase, p->d_subs, p->d_err, p->d_grid, p->d_grid_in, p->d_grid_adj, p->d_beta64,
                   p->d_betaT, p->d_poly, p->d_stage_grid, p->d_stage_nodes, p->d_stage_nodes2, p->d_stage_grid2, p->d_cnt, p->d_tile_total,
                   p->d_ticket, p->d_perm, p->d_kc, p->d_jc, p->d_cstart, p->d_ccount, p->d_cslot,
-                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT, p->d_fc, p->d_cl, p->d_inv};
+                  p->d_scan_status, p->d_ctr, p->d_big, p->d_wt, p->d_fT, p->d_fc, p->d_cl, p->d_inv, p->d_bw,
+                  p->d_bi};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->fft_ok) cufftDestroy(p->fft);
@@ -372,6 +378,8 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
                cudaSuccess &&
            cudaFuncSetAttribute((const void*)ks.interp1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib) ==
                cudaSuccess &&
+           cudaFuncSetAttribute((const void*)ks.interp1t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib) ==
+               cudaSuccess &&
            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void*)ks.spread1, S1_THREADS, sb) == cudaSuccess &&
            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, (const void*)ks.spread1t, S1_THREADS, sb) == cudaSuccess &&
            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp1, I1_THREADS, ib) == cudaSuccess &&
@@ -399,6 +407,8 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
       const bool interp_ok = nrows <= 1024 && p->region_bytes <= 200 * 1024 &&
                              cudaFuncSetAttribute((const void*)ks.interp_cell, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)p->region_bytes) == cudaSuccess &&
+                             cudaFuncSetAttribute((const void*)ks.interp_cellt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)p->region_bytes) == cudaSuccess &&
                              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, (const void*)ks.interp_cell, RC_THREADS,
                                                                            p->region_bytes) == cudaSuccess &&
                              occ_i >= 1;
@@ -409,13 +419,13 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
               occ_s >= 1;
       // the spread_cell fallback's limits only matter when neither the warp-block nor the batch adjoint
       // takes the plan (checked again below, after those are configured)
-      ok = interp_ok && (sc_ok || p->wbmode || p->batchmode);
+      ok = interp_ok && (sc_ok || p->wbmode || p->batchmode || p->full);
       p->sc_cap = cap;
       p->sc_bytes = sb;
     }
     cudaGetLastError();
     p->cellmode = ok;
-    if (!ok) p->tensor = false;
+    if (!ok) p->tensor = p->full = false;
   }
   if (p->batchmode) {
     bool ok = p->cellmode && ks.spread_rowbatch;
@@ -445,9 +455,9 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
     p->wbmode = ok;
   }
-  if (p->cellmode && p->D >= 2 && !p->wbmode && !p->batchmode && !sc_ok) {  // no adjoint for this tile in cell mode
+  if (p->cellmode && p->D >= 2 && !p->wbmode && !p->batchmode && !p->full && !sc_ok) {  // no cell-mode adjoint
     p->cellmode = false;
-    p->tensor = false;
+    p->tensor = p->full = false;
   }
   p->use_ind = false;
   if (p->D >= 2 && !p->cellmode && p->tiled && ks.interp_nd &&
@@ -602,7 +612,8 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
   if (p->cellmode) {
     TRY(cell_sort<R>(p, st));
     p->tile_binned = false;
-    if (p->batchmode || p->wbmode) {  // taps of every node for the D >= 2 adjoint (TENSOR layout)
+    if (p->batchmode || p->wbmode || (p->tensor && p->D >= 2)) {
+      // taps of every node for the D >= 2 adjoint / the TENSOR strategy (layout wt[pos][d][t])
       const KernelSet<R>& ks = kernels_of<R>(p);
       CK(launch_k(ks.taps_nd, (unsigned)((p->M + TN_NODES - 1) / TN_NODES), TN_NODES, 0, st, p->geom, WpnArg{p->wpn},
                   (const R*)p->d_kc, (R*)p->d_wt, p->wbmode ? p->d_cl : (int*)nullptr));
@@ -613,7 +624,13 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
         CKL();
       }
     }
-    if (p->tensor) {  // TENSOR strategy: the 2m taps of every node, in cell order
+    if (p->full) {  // FULL strategy: the rows of B (weights, grid indices) in cell order
+      const KernelSet<R>& ks = kernels_of<R>(p);
+      CK(launch_k(ks.full_build, (unsigned)((p->M + FB_NODES - 1) / FB_NODES), FB_THREADS, 0, st, p->geom,
+                  WpnArg{p->wpn}, (const R*)p->d_kc, (R*)p->d_bw, p->d_bi, p->D >= 2 ? p->d_cl : (int*)nullptr));
+      ++p->launches;
+    }
+    if (p->tensor && p->D == 1) {  // TENSOR strategy: the 2m taps of every node, in cell order
       const KernelSet<R>& ks = kernels_of<R>(p);
       CK(launch_k(ks.taps1, (unsigned)((p->M + T1_THREADS - 1) / T1_THREADS), T1_THREADS, 0, st, p->geom, WpnArg{p->wpn},
                   (const R*)p->d_kc, (R*)p->d_wt));
@@ -676,16 +693,24 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
   (void)wp;
   const WpnArg wpn{p->wpn};
   const auto* grid = (const typename cplx<T>::type*)p->d_grid;
-  if (p->cellmode && p->D >= 2) {
-    CK(launch_k(ks.interp_cell, dim3((unsigned)p->n_tiles, (unsigned)p->B), RC_THREADS, p->region_bytes, st, p->geom, wpn,
-                grid, (const T*)p->d_kc, (const int*)p->d_jc, (const int*)p->d_cstart, p->node_begin, p->node_end, f));
+  if (p->full) {  // f = B ghat over the stored rows
+    const unsigned npb = FI_THREADS / (p->full_e <= 16 ? 8 : 32);
+    const unsigned ctas = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p->node_end - p->node_begin + npb - 1) / npb,
+                                                                           (int64_t)p->sm_count * 16));
+    CK(launch_k(ks.full_interp, dim3(ctas, (unsigned)p->B), FI_THREADS, 0, st, p->geom, grid, (const T*)p->d_bw,
+                (const int*)p->d_bi, (const int*)p->d_jc, p->node_begin, p->node_end, f));
+  } else if (p->cellmode && p->D >= 2) {
+    CK(launch_k(p->tensor ? ks.interp_cellt : ks.interp_cell, dim3((unsigned)p->n_tiles, (unsigned)p->B), RC_THREADS,
+                p->region_bytes, st, p->geom, wpn, grid, (const T*)p->d_kc, (const T*)p->d_wt, (const int*)p->d_jc,
+                (const int*)p->d_cstart, p->node_begin, p->node_end, f));
   } else if (p->use_ind) {
     ks.interp_nd<<<(unsigned)p->n_tiles, RN_THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
   } else if (p->cellmode && p->D == 1) {
     const unsigned segs = (unsigned)((p->Nt[0] + I1_SEG - 1) / I1_SEG);
-    CK(launch_k(ks.interp1, dim3(segs, (unsigned)p->B), I1_THREADS, p->r1_interp_bytes, st, p->geom, wpn, grid,
-                (const T*)p->d_kc, (const int*)p->d_jc, (const int*)p->d_cstart, p->node_begin, p->node_end, f));
+    CK(launch_k(p->tensor ? ks.interp1t : ks.interp1, dim3(segs, (unsigned)p->B), I1_THREADS, p->r1_interp_bytes, st,
+                p->geom, wpn, grid, (const T*)p->d_kc, (const T*)p->d_wt, (const int*)p->d_jc, (const int*)p->d_cstart,
+                p->node_begin, p->node_end, f));
   } else if (p->tiled) {
     ks.interp_tiled<<<p->grid_tiled, THREADS, p->region_bytes, st>>>(
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_subs, p->d_subbase + p->n_tiles, f);
@@ -703,6 +728,19 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   auto* grid = (typename cplx<T>::type*)p->d_grid_adj;  // all zero on entry (plan creation / previous crop)
+  if (p->full && p->D >= 2) {
+    // ghat = B^H f: values in cell order, then one thread per oversampled cell over the stored weights
+    rec(p, 1, 1);
+    using C = typename cplx<T>::type;
+    permute_f_kernel<T><<<dim3((unsigned)((p->M + 1023) / 1024), (unsigned)p->B), 256, 0, st>>>(
+        f, p->d_jc, (int)p->M, p->node_begin, p->node_end, (C*)p->d_fc);
+    CKL();
+    const unsigned ctas = (unsigned)std::min<int64_t>((p->ncells + FS_THREADS - 1) / FS_THREADS, (int64_t)p->sm_count * 16);
+    CK(launch_k(ks.full_spread, dim3(ctas, (unsigned)p->B), FS_THREADS, 0, st, p->geom, (const C*)p->d_fc,
+                (const int*)p->d_cl, (const T*)p->d_bw, (const int*)p->d_cstart, grid));
+    p->launches += 2;
+    return NFFT_SUCCESS;
+  }
   if (p->batchmode) {
     using C = typename cplx<T>::type;
     rec(p, 1, 1);
@@ -747,8 +785,10 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     rec(p, 1, 1);
     const unsigned segs = std::min<unsigned>((unsigned)((p->Nt[0] + S1_SEG - 1) / S1_SEG),
                                              (unsigned)(S1_CTAS_PER_SM * p->sm_count));
-    CK(launch_k(p->tensor ? ks.spread1t : ks.spread1, dim3(segs, (unsigned)p->B), S1_THREADS, p->r1_spread_bytes, st,
-                p->geom, WpnArg{p->wpn}, f, (const T*)p->d_kc, (const T*)p->d_wt, (const int*)p->d_jc,
+    // FULL in 1D: the rows of B are the 2m taps, so the TENSOR kernel reads them
+    CK(launch_k((p->tensor || p->full) ? ks.spread1t : ks.spread1, dim3(segs, (unsigned)p->B), S1_THREADS,
+                p->r1_spread_bytes, st, p->geom, WpnArg{p->wpn}, f, (const T*)p->d_kc,
+                (const T*)(p->full ? p->d_bw : p->d_wt), (const int*)p->d_jc,
                 (const int*)p->d_cstart, p->node_begin, p->node_end, grid));
     ++p->launches;
     CKL();
@@ -995,7 +1035,7 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   if (opt.batch < 1) return NFFT_ERROR_INVALID_VALUE;
   if (opt.batch > 65535) return NFFT_ERROR_UNSUPPORTED;  // batch vectors index grid dimension y
   if (opt.method < 0 || opt.method > 7) return NFFT_ERROR_INVALID_VALUE;
-  if (opt.precompute < NFFT_PRECOMPUTE_AUTO || opt.precompute > NFFT_PRECOMPUTE_TENSOR) return NFFT_ERROR_INVALID_VALUE;
+  if (opt.precompute < NFFT_PRECOMPUTE_AUTO || opt.precompute > NFFT_PRECOMPUTE_FULL) return NFFT_ERROR_INVALID_VALUE;
   if (!(sigma > 1.0) || !std::isfinite(sigma)) return NFFT_ERROR_BAD_GEOMETRY;
   if (m > MAX_M) return NFFT_ERROR_UNSUPPORTED;
   if (M > (int64_t)0x7fffffff - 1) return NFFT_ERROR_UNSUPPORTED;
@@ -1184,23 +1224,30 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
          alloc((void**)&p->d_scan_status, (size_t)((cells + CL_SCAN_TILE - 1) / CL_SCAN_TILE + 1) * 8) &&
          alloc((void**)&p->d_ctr, 16) &&
          alloc((void**)&p->d_big, (size_t)(M / (CL_SMALL + 1) + 1) * 4);
-  // TENSOR precompute: the D = 1 cell-mode adjoint, on request (AUTO = POLYNOMIAL: measured
-  // faster on B200)
-  p->tensor = p->cellmode && D == 1 && opt.precompute == NFFT_PRECOMPUTE_TENSOR;
-  if (ok && p->tensor) ok = alloc(&p->d_wt, (size_t)M * 2 * m * rs);
+  // window precompute strategies (AUTO = POLYNOMIAL, measured fastest on B200):
+  // TENSOR stores the 2m D taps of every node (all kernels read them), FULL the rows of the sparse matrix B
+  p->tensor = p->cellmode && opt.precompute == NFFT_PRECOMPUTE_TENSOR;
+  p->full = p->cellmode && opt.precompute == NFFT_PRECOMPUTE_FULL;
+  p->full_e = 1;
+  for (int d = 0; d < D; ++d) p->full_e *= 2 * m;
+  if (ok && p->tensor) ok = alloc(&p->d_wt, (size_t)M * D * 2 * m * rs);
+  if (ok && p->full) {
+    ok = alloc(&p->d_bw, (size_t)M * p->full_e * rs) && alloc((void**)&p->d_bi, (size_t)M * p->full_e * 4);
+    if (ok && D >= 2) ok = alloc(&p->d_fc, (size_t)M * p->B * csz) && alloc((void**)&p->d_cl, (size_t)M * 4);
+  }
   // 2D batches of >= 8 transforms: row-segment adjoint with lanes = batch vectors (not for node
   // shards; the 16 + 2m - 1 window columns must not wrap onto themselves)
-  p->batchmode = p->cellmode && D == 2 && p->B >= 8 && opt.node_begin == 0 && (opt.node_end == 0 || opt.node_end == M) &&
-                 Nt[1] >= RB_SEG + 2 * m - 1;
+  p->batchmode = p->cellmode && !p->full && D == 2 && p->B >= 8 && opt.node_begin == 0 &&
+                 (opt.node_end == 0 || opt.node_end == M) && Nt[1] >= RB_SEG + 2 * m - 1;
   p->bp = (int)((p->B + 31) / 32 * 32);
   if (ok && p->batchmode)
-    ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && alloc(&p->d_wt, (size_t)M * D * 2 * m * rs) &&
+    ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && (p->d_wt || alloc(&p->d_wt, (size_t)M * D * 2 * m * rs)) &&
          alloc((void**)&p->d_inv, (size_t)M * 4);
   // D = 2, 3 (not batched): warp-block adjoint over the TENSOR taps; the last-dimension window
   // (32 or 8 lanes + 2m - 1 cells) must not wrap onto itself
-  p->wbmode = p->cellmode && !p->batchmode && D >= 2 && Nt[D - 1] >= (D == 3 ? 8 : 32) + 2 * m - 1;
+  p->wbmode = p->cellmode && !p->full && !p->batchmode && D >= 2 && Nt[D - 1] >= (D == 3 ? 8 : 32) + 2 * m - 1;
   if (ok && p->wbmode)
-    ok = alloc(&p->d_wt, (size_t)M * D * 2 * m * rs) && alloc(&p->d_fc, (size_t)M * p->B * csz) &&
+    ok = (p->d_wt || alloc(&p->d_wt, (size_t)M * D * 2 * m * rs)) && alloc(&p->d_fc, (size_t)M * p->B * csz) &&
          alloc((void**)&p->d_cl, (size_t)M * 4);
   if (!ok) return fail(NFFT_ERROR_OUT_OF_MEMORY);
   {
@@ -1579,6 +1626,7 @@ nfft_status nfft_get_stage_times(nfft_plan p, int which, float* ms) {
 nfft_status nfft_get_features(nfft_plan p, int* features) {
   if (!p || !features) return NFFT_ERROR_INVALID_VALUE;
   *features = (p->cellmode ? NFFT_FEATURE_CELL_MODE : 0) | (p->tensor ? NFFT_FEATURE_TENSOR : 0) |
+              (p->full ? NFFT_FEATURE_FULL : 0) |
               (p->batchmode ? NFFT_FEATURE_BATCH : 0) | (p->wbmode ? NFFT_FEATURE_WBLOCK : 0);
   return NFFT_SUCCESS;
 }

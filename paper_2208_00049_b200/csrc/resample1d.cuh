@@ -47,10 +47,11 @@ __host__ __device__ inline size_t i1_smem_bytes(int M, size_t csize) {
   return (((size_t)I1_SEG + 2 * M) * csize + 15) & ~(size_t)15;
 }
 
-template <typename T, int M, int DEG>
+template <typename T, int M, int DEG, bool TENSOR>
 __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T, 1, M> wp,
                                                               const typename cplx<T>::type* __restrict__ grid,
-                                                              const T* __restrict__ kc, const int* __restrict__ jc,
+                                                              const T* __restrict__ kc, const T* __restrict__ wt,
+                                                              const int* __restrict__ jc,
                                                               const int* __restrict__ cstart, int nb, int ne,
                                                               typename cplx<T>::type* __restrict__ f) {
   using C = typename cplx<T>::type;
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
   for (int i = 0; i < I1_U; ++i) {
     const int p = p0 + threadIdx.x + i * I1_THREADS;
     jj[i] = -1;
+    kk[i] = 0.0;
     if (p < p1) {
       kk[i] = (double)kc[p];
       jj[i] = jc[p];
@@ -96,11 +98,16 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
   __syncthreads();
   NFFTB_TRACE(1);
   C* fb = f + (long long)b * g.M;
-  auto one = [&](double k, int j) {
+  auto one = [&](double k, int j, int p) {
     double frac;
     const int c = node_cell(k, g.Ntd[0], Nt, frac);  // c in [y0, y0 + nseg): footprint starts at window cell c - y0
     T w[TAPS];
-    window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
+    if constexpr (TENSOR) {  // the stored taps of position p
+#pragma unroll
+      for (int l = 0; l < TAPS; ++l) w[l] = __ldg(wt + (long long)p * TAPS + l);
+    } else {
+      window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
+    }
     const C* row = sg + (c - y0);
     C acc;
     acc.x = (T)0;
@@ -115,9 +122,9 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
   };
 #pragma unroll
   for (int i = 0; i < I1_U; ++i)
-    if (jj[i] >= 0) one(kk[i], jj[i]);
+    if (jj[i] >= 0) one(kk[i], jj[i], p0 + threadIdx.x + i * I1_THREADS);
   // dense segments: the remaining nodes
-  for (int p = p0 + threadIdx.x + I1_U * I1_THREADS; p < p1; p += I1_THREADS) one((double)kc[p], jc[p]);
+  for (int p = p0 + threadIdx.x + I1_U * I1_THREADS; p < p1; p += I1_THREADS) one((double)kc[p], jc[p], p);
   __syncthreads();  // the next segment overwrites the staged index set
   }  // segments
   NFFTB_TRACE(2);

@@ -37,10 +37,11 @@ constexpr int RC_THREADS = 256;  // interp_cell
 constexpr int SC_K = 4;          // spread_cell: consecutive last-dimension cells per thread
 
 // ---------------------------------------------------------------- forward
-template <typename T, int D, int M, int DEG>
+template <typename T, int D, int M, int DEG, bool TENSOR>
 __global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel(Geom g, WinPolyN<T, D, M> wp,
                                                                  const typename cplx<T>::type* __restrict__ grid,
-                                                                 const T* __restrict__ kc, const int* __restrict__ jc,
+                                                                 const T* __restrict__ kc, const T* __restrict__ wt,
+                                                                 const int* __restrict__ jc,
                                                                  const int* __restrict__ cstart, int nb, int ne,
                                                                  typename cplx<T>::type* __restrict__ f) {
   using C = typename cplx<T>::type;
@@ -156,7 +157,12 @@ __global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel
     for (int d = 0; d < D; ++d) {
       double frac;
       loc[d] = node_cell((double)kc[(long long)d * g.M + pos], g.Ntd[d], g.Nt[d], frac) - c0[d];
-      window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w[d]);
+      if constexpr (TENSOR) {  // the stored taps wt[pos][d][t]
+#pragma unroll
+        for (int t = 0; t < 2 * M; ++t) w[d][t] = __ldg(wt + ((long long)pos * D + d) * 2 * M + t);
+      } else {
+        window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[d], w[d]);
+      }
     }
   };
   auto eval = [&](const int (&loc)[D], const T (&w)[D][2 * M]) {

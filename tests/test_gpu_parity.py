@@ -495,27 +495,92 @@ def test_cell_binning_bit_exact(config):
     np.testing.assert_array_equal(cstart, ref_offs)
 
 
-@pytest.mark.parametrize("precompute", ["polynomial", "tensor"])
-@pytest.mark.parametrize("case", ["small", "ragged_batch", "dense_cells", "full"])
-def test_1d_precompute_strategies(precompute, case):
-    """D = 1 cell mode with the POLYNOMIAL (taps per call) and TENSOR (taps stored
-    by nfft_precompute) strategies against the oracle: small
-    grid whose spread window wraps the torus several times, batch + ragged
-    tile, many coincident nodes (cells with > 8 nodes), full BASELINE size."""
-    if case == "small":
+STRATEGY_CASES = ["1d_small", "1d_ragged_batch", "1d_dense_cells", "1d_full_size", "2d_c128_m5", "2d_c64_batch3",
+                  "2d_batch9_c64", "2d_wrap_m8", "2d_full_size", "3d_c128_m3", "3d_c64_ragged", "3d_full_size",
+                  "radial_b32_s125_full_size"]
+
+
+@pytest.mark.parametrize("precompute", ["polynomial", "tensor", "full"])
+@pytest.mark.parametrize("case", STRATEGY_CASES)
+def test_precompute_strategies(precompute, case):
+    """The window precomputation strategies (§3.7) through the
+    cell-mode kernels against the oracle: POLYNOMIAL (taps per call), TENSOR
+    (2m D taps per node stored, every kernel reads them), FULL (the sparse
+    matrix B stored: SpMV forward, owner-computes gather adjoint). Small grids
+    whose windows wrap the torus, batches, cells with > 8 nodes, c64 / c128,
+    and the BASELINE sizes (config 2, 3, 4 and the radial batch)."""
+    tile = None
+    if case == "1d_small":
         w = workloads.make("cfg1_1d_256", seed=3, N=(20,), M=70, m=4)
-    elif case == "ragged_batch":
+    elif case == "1d_ragged_batch":
         w = workloads.make("cfg1_1d_256", seed=4, N=(300,), M=700, m=5, batch=3)
-    elif case == "dense_cells":
+        tile = (96,)
+    elif case == "1d_dense_cells":
         w = workloads.make("cfg1_1d_256", seed=5, N=(64,), M=600, m=3)
         w["nodes"] = np.round(w["nodes"] * 16) / 16  # 16 distinct on-grid positions
-    else:
+    elif case == "1d_full_size":
         w = workloads.make("cfg2_1d_2e18", seed=0, m=4)
-    plan = _plan(w, precompute=precompute)
-    feats = plan.features()
-    plan.close()
-    assert "cell_mode" in feats and (("tensor" in feats) == (precompute == "tensor")), feats
-    _check(w, precompute=precompute)
+    elif case == "2d_c128_m5":
+        w = workloads.make("cfg3_2d_512", seed=71, N=(48, 40), M=2500, m=5)
+        tile = (20, 14)
+    elif case == "2d_c64_batch3":
+        w = workloads.make("cfg5_radial_s2", seed=72, N=(40, 36), M=1200, m=4, batch=3)
+    elif case == "2d_batch9_c64":
+        w = workloads.make("cfg5_radial_s2", seed=73, N=(40, 48), M=1400, m=4, batch=9)
+    elif case == "2d_wrap_m8":
+        w = workloads.make("cfg3_2d_512", seed=74, N=(18, 20), M=300, m=8)
+    elif case == "2d_full_size":
+        w = workloads.make("cfg3_2d_512", seed=0, m=4)
+    elif case == "3d_c128_m3":
+        w = workloads.make("cfg4_3d_64", seed=75, N=(12, 14, 12), M=1500, m=3)
+    elif case == "3d_c64_ragged":
+        w = workloads.make("cfg4_3d_64", seed=76, N=(10, 12, 14), M=1200, m=2)
+        w = dict(w, nodes=w["nodes"].astype(np.float32), fhat=w["fhat"].astype(np.complex64),
+                 f=w["f"].astype(np.complex64), precision="c64")
+        tile = (6, 5, 7)
+    elif case == "3d_full_size":
+        w = workloads.make("cfg4_3d_64", seed=0, m=4)
+    else:
+        w = workloads.make("cfg5_radial_s125", seed=0)
+    kw = dict(precompute=precompute)
+    if tile:
+        kw["tile"] = tile
+    feats = _check_features(w, **kw)
+    assert "cell_mode" in feats, feats
+    assert ("tensor" in feats) == (precompute == "tensor") and ("full" in feats) == (precompute == "full"), feats
+    if case == "radial_b32_s125_full_size":
+        got_f, got_y, _ = _run(w, **kw)
+        rf, ry = _oracle(w, range(0, 32, 5))
+        for i, b in enumerate(range(0, 32, 5)):
+            assert rel_l2(got_f[b], rf[i]) <= 2e-5 and rel_l2(got_y[b], ry[i]) <= 2e-5, b
+    else:
+        _check(w, **kw)
+
+
+@pytest.mark.parametrize("precompute", ["tensor", "full"])
+@pytest.mark.parametrize("D", [1, 2, 3])
+def test_strategy_shards_sum_to_full_transform(precompute, D):
+    """Node shards (options.node_begin/end over the cell-sorted order) with the
+    stored-table strategies: the shards' forward outputs cover disjoint nodes
+    and their adjoints sum to the full adjoint (linearity)."""
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    from paper_2208_00049_b200 import dist
+    w = {1: workloads.make("cfg2_1d_2e18", seed=81, N=(400,), M=900, m=4),
+         2: workloads.make("cfg3_2d_512", seed=82, N=(36, 40), M=1500, m=4),
+         3: workloads.make("cfg4_3d_64", seed=83, N=(12, 12, 12), M=1200, m=3)}[D]
+    rf, ry = _oracle(w)
+    nodes = torch.from_numpy(w["nodes"]).cuda()
+    acc_f = np.zeros((1, w["M"]), complex)
+    acc_y = np.zeros((1,) + tuple(w["N"]), complex)
+    for rank in range(3):
+        plan = pkg.NfftPlan(nodes, w["N"], m=w["m"], precompute=precompute,
+                            node_range=dist.shard_range(w["M"], rank, 3)).precompute()
+        out = torch.zeros((1, w["M"]), dtype=torch.complex128, device="cuda")
+        acc_f += plan.forward(torch.from_numpy(w["fhat"]).cuda(), out=out).cpu().numpy()
+        acc_y += plan.adjoint(torch.from_numpy(w["f"]).cuda()).cpu().numpy()
+        plan.close()
+    assert rel_l2(acc_f[0], rf[0]) <= 1e-12 and rel_l2(acc_y[0], ry[0]) <= 1e-12
 
 
 @pytest.mark.parametrize("case", ["2d_c64_b32", "2d_c128_b9", "radial_b33_s125", "2d_c64_b8_m8"] +
