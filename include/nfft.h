@@ -220,10 +220,16 @@ nfft_status nfft_get_cell_binning(nfft_plan p, int32_t* order_host, int32_t* cst
  * [d][tap][z]); *deg receives the polynomial degree. Synchronises. */
 nfft_status nfft_get_window_tables(nfft_plan p, double* beta_tensor, double* poly, int* deg);
 
-/* Milliseconds of the most recent forward/adjoint stages (timing = 1):
+/* Milliseconds of the stages of the most recent nfft_forward / nfft_adjoint
+ * call, whichever ran last (timing = 1): deconvolution + pad (or
+ * crop + deconvolution), cuFFT, resampling kernel. Any pointer may be NULL.
+ * Synchronises. NFFT_ERROR_INVALID_VALUE when the plan was created without timing. */
+nfft_status nfft_get_stage_times(nfft_plan p, float* ms_deconv, float* ms_fft, float* ms_resample);
+
+/* All five stage times of the most recent forward (which = 0) or adjoint (1):
  * ms[0] deconv/pad or crop/deconv, ms[1] cuFFT, ms[2] resampling kernel,
- * ms[3] grid zeroing (adjoint), ms[4] precompute. Synchronises. */
-nfft_status nfft_get_stage_times(nfft_plan p, int which /* 0 forward, 1 adjoint */, float* ms5);
+ * ms[3] grid zeroing (adjoint; 0 in cell mode), ms[4] precompute. Synchronises. */
+nfft_status nfft_get_stage_times_ex(nfft_plan p, int which /* 0 forward, 1 adjoint */, float* ms5);
 
 /* Number of this library's own kernel launches since plan creation
  * (cuFFT's kernels are not counted). */

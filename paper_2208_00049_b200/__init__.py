@@ -26,6 +26,7 @@ NFFT_SYMBOLS = (
     "nfft_default_options", "nfft_plan_create", "nfft_plan_create_ex", "nfft_set_nodes",
     "nfft_precompute", "nfft_forward", "nfft_adjoint", "nfft_plan_destroy", "nfft_status_string",
     "nfft_plan_info", "nfft_get_binning", "nfft_get_window_tables", "nfft_get_stage_times",
+    "nfft_get_stage_times_ex",
     "nfft_get_launch_count", "nfft_run_stage", "nfft_execute", "nfft_get_cell_binning", "nfft_get_features",
     "nfft_autotune_tile",
 )
@@ -85,7 +86,8 @@ def lib():
         "nfft_get_binning": [vp, P(i32), P(i32)],
         "nfft_get_cell_binning": [vp, P(i32), P(i32)],
         "nfft_get_window_tables": [vp, P(ctypes.c_double), P(ctypes.c_double), P(c_int)],
-        "nfft_get_stage_times": [vp, c_int, P(ctypes.c_float)],
+        "nfft_get_stage_times": [vp, P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float)],
+        "nfft_get_stage_times_ex": [vp, c_int, P(ctypes.c_float)],
         "nfft_get_launch_count": [vp, P(i64)],
         "nfft_get_features": [vp, P(c_int)],
         "nfft_autotune_tile": [c_int, P(i64), i64, vp, ctypes.c_double, c_int, c_int, vp, P(i64), c_int, c_int,
@@ -355,7 +357,7 @@ class NfftPlan:
 
     def stage_times(self, which):
         ms = (ctypes.c_float * 5)()
-        _check(lib().nfft_get_stage_times(self._h, 0 if which == "forward" else 1, ms), "nfft_get_stage_times")
+        _check(lib().nfft_get_stage_times_ex(self._h, 0 if which == "forward" else 1, ms), "nfft_get_stage_times_ex")
         return dict(deconv=ms[0], fft=ms[1], resample=ms[2], zero=ms[3], precompute=ms[4])
 
     def features(self):

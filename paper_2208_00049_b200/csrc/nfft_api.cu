@@ -139,6 +139,7 @@ struct nfft_plan_s {
   bool precomputed = false;
   cudaEvent_t ev[3][6] = {};
   bool events = false;
+  int last_dir = 0;          // 0 forward, 1 adjoint: the most recent call (nfft_get_stage_times)
   int64_t launches = 0;
   size_t csize() const { return prec == NFFT_COMPLEX128 ? 16 : 8; }
   size_t rsize() const { return prec == NFFT_COMPLEX128 ? 8 : 4; }
@@ -872,6 +873,7 @@ nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
     if (!p->d_stage_nodes) CK(cudaMalloc(&p->d_stage_nodes, node_bytes));
     f = (C*)p->d_stage_nodes;
   }
+  p->last_dir = 0;
   rec(p, 0, 0);
   TRY(stage_deconv<T>(p, fhat, p->stream));
   rec(p, 0, 1);
@@ -904,6 +906,7 @@ nfft_status adjoint_impl(nfft_plan p, const void* f_in, void* y_out) {
     if (!p->d_stage_grid) CK(cudaMalloc(&p->d_stage_grid, grid_bytes_out));
     y = (C*)p->d_stage_grid;
   }
+  p->last_dir = 1;
   rec(p, 1, 0);
   TRY(stage_spread<T>(p, f, p->stream));
   rec(p, 1, 2);
@@ -1595,7 +1598,7 @@ nfft_status nfft_get_window_tables(nfft_plan p, double* beta_tensor, double* pol
   return NFFT_SUCCESS;
 }
 
-nfft_status nfft_get_stage_times(nfft_plan p, int which, float* ms) {
+nfft_status nfft_get_stage_times_ex(nfft_plan p, int which, float* ms) {
   if (!p || !ms || which < 0 || which > 1) return NFFT_ERROR_INVALID_VALUE;
   if (!p->events) return NFFT_ERROR_INVALID_VALUE;
   DeviceGuard guard(p->device);
@@ -1620,6 +1623,19 @@ nfft_status nfft_get_stage_times(nfft_plan p, int which, float* ms) {
     ms[0] = el(1, 3, 4);
   }
   ms[4] = el(2, 0, 1);
+  return NFFT_SUCCESS;
+}
+
+// SURVEY §8(b)'s form: the deconvolution (or crop), FFT and resampling times of
+// the most recent forward or adjoint call (whichever ran last).
+nfft_status nfft_get_stage_times(nfft_plan p, float* ms_deconv, float* ms_fft, float* ms_resample) {
+  if (!p) return NFFT_ERROR_INVALID_VALUE;
+  float ms[5];
+  nfft_status s = nfft_get_stage_times_ex(p, p->last_dir, ms);
+  if (s != NFFT_SUCCESS) return s;
+  if (ms_deconv) *ms_deconv = ms[0];
+  if (ms_fft) *ms_fft = ms[1];
+  if (ms_resample) *ms_resample = ms[2];
   return NFFT_SUCCESS;
 }
 

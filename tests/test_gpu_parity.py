@@ -857,3 +857,26 @@ def test_odd_n(case):
         w = workloads.make("cfg3_2d_512", seed=66, N=(23, 31), M=800, m=4)
         kw = dict(method="direct")
     _check(w, **kw)
+
+
+def test_stage_times():
+    """timing = 1: nfft_get_stage_times (deconv, FFT, resampling of
+    the most recent call) and nfft_get_stage_times_ex (all five per direction)."""
+    torch = _torch()
+    import ctypes
+    import paper_2208_00049_b200 as pkg
+    w = workloads.make("cfg3_2d_512", seed=91, N=(64, 64), M=3000, m=4)
+    plan = _plan(w, timing=True)
+    plan.forward(torch.from_numpy(w["fhat"]).cuda())
+    ms = [ctypes.c_float() for _ in range(3)]
+    assert pkg.lib().nfft_get_stage_times(plan._h, *[ctypes.byref(x) for x in ms]) == 0
+    assert all(x.value > 0 for x in ms), [x.value for x in ms]
+    plan.adjoint(torch.from_numpy(w["f"]).cuda())
+    assert pkg.lib().nfft_get_stage_times(plan._h, *[ctypes.byref(x) for x in ms]) == 0
+    st = plan.stage_times("adjoint")
+    assert abs(st["resample"] - ms[2].value) < 1e-6 and st["resample"] > 0 and st["fft"] > 0
+    assert plan.stage_times("forward")["deconv"] > 0
+    plan.close()
+    nt = _plan(w)
+    assert pkg.lib().nfft_get_stage_times(nt._h, None, None, None) == 1  # no timing events
+    nt.close()

@@ -92,8 +92,8 @@ def main():
     tag = sys.argv[3] if len(sys.argv) > 3 else os.path.basename(dst.rstrip("/"))
     cfg = sys.argv[4] if len(sys.argv) > 4 else "cfg2_1d_2e18:m4"
     os.makedirs(dst, exist_ok=True)
-    header = ("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 3 "
-              "--warmup 3 --no-sweep --no-e2e --no-cpu")
+    header = ("# ncu --metrics gpu__time_duration.sum --clock-control none -c 600 python bench.py --steps 3 "
+              "--warmup 3 --no-sweep --no-e2e --no-cpu --no-configs --no-strategies (tools/gpu_evidence.sh)")
     if os.path.exists(os.path.join(src, "launches.csv")):
         launches(src, dst, tag, header)
     if os.path.exists(os.path.join(src, "full_raw.csv")):
