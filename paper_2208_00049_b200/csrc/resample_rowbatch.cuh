@@ -30,7 +30,10 @@
 
 namespace nfftb {
 
-constexpr int RB_THREADS = 256;  // 8 warps
+#ifndef RB_NWARPS
+#define RB_NWARPS 8
+#endif
+constexpr int RB_THREADS = 32 * RB_NWARPS;  // warps per CTA (the 2m window rows are dealt round-robin)
 constexpr int RB_LANES = 32;     // vectors per chunk
 constexpr int RB_SEG = 16;       // cells per CTA (last dimension)
 constexpr int RB_PITCH = 33;     // partial-row pitch in shared memory (vectors + 1)
@@ -189,7 +192,7 @@ __device__ __forceinline__ void rb_row(int lo_l, int hi_l, int lead, const typen
 // (per-cell ranges from cstart, lane u holds column u's), then the warps'
 // partial rows are summed in shared memory and stored coalesced.
 template <typename T, int M>
-__global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_rowbatch_kernel(
+__global__ void __launch_bounds__(RB_THREADS) spread_rowbatch_kernel(
     Geom g, const typename cplx<T>::type* __restrict__ fTc, int BP, const T* __restrict__ wt,
     const int* __restrict__ cstart, typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
@@ -213,10 +216,15 @@ __global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_row
   }
   fTc += b0 + lane;
   for (int r = warp; r < TAPS; r += NW) {  // window row x0 = y0 - m + r
-    const long long rowkey = (long long)pos_mod(y0 - M + r, Nt0) * NtL;
+    int xr = y0 - M + r;  // in (-Nt0, 2 Nt0): one conditional wrap
+    if (xr < 0) xr += Nt0;
+    else if (xr >= Nt0) xr -= Nt0;
+    const long long rowkey = (long long)xr * NtL;
     int lo_l = 0, hi_l = 0;
     if (lane < WC) {  // window column u = lane: binning column c0 - m + u
-      const int col = pos_mod(c0 - M + lane, NtL);
+      int col = c0 - M + lane;
+      if (col < 0) col += NtL;
+      else if (col >= NtL) col -= NtL;
       lo_l = __ldg(cstart + rowkey + col);
       hi_l = __ldg(cstart + rowkey + col + 1);
     }
@@ -228,7 +236,11 @@ __global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_row
   for (int k = 0; k < RB_SEG; ++k) part[((size_t)warp * RB_SEG + k) * RB_PITCH + lane] = acc[k];
   __syncthreads();
   const int nbc = min(RB_LANES, g.B - b0);
-  const long long rowoff = (long long)pos_mod(y0 - (Nt0 >> 1), Nt0) * NtL;
+  int ys = y0 - (Nt0 >> 1);
+  if (ys < 0) ys += Nt0;
+  const long long rowoff = (long long)ys * NtL;
+  int cs0 = c0 - (NtL >> 1);
+  if (cs0 < 0) cs0 += NtL;
   for (int idx = tid; idx < nbc * RB_SEG; idx += RB_THREADS) {
     const int bb = idx / RB_SEG, k = idx - bb * RB_SEG;
     if (k >= qs) continue;
@@ -241,7 +253,9 @@ __global__ void __launch_bounds__(RB_THREADS, sizeof(T) == 4 ? 4 : 2) spread_row
       a.x += c.x;
       a.y += c.y;
     }
-    grid[(long long)(b0 + bb) * g.grid_cells + rowoff + pos_mod(c0 + k - (NtL >> 1), NtL)] = a;
+    int cs = cs0 + k;
+    if (cs >= NtL) cs -= NtL;
+    grid[(long long)(b0 + bb) * g.grid_cells + rowoff + cs] = a;
   }
 }
 
