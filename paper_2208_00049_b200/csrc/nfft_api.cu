@@ -1069,12 +1069,14 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     // 2D 32 x 64 measured fastest for it where Ntilde_1 >= 512 (512^2: 23.1 -> 20.9 us, radial
     // sigma = 2: 244 -> 230 us), 32 x 32 on smaller grids (radial sigma = 1.25, 320^2: 64 wide
     // tiles leave too few CTAs around the dense centre: 196 -> 240 us)
-    // batches of >= 8 vectors (per-vector interp CTAs): 16 rows per tile (radial sigma = 1.25:
-    // 195 -> 184 us, sigma = 2: 230 -> 226 us)
+    // batches of >= 8 vectors (per-vector interp CTAs): 8 rows x the row split into equal parts of
+    // <= 256 cells (radial sigma = 2: 16 x 64 228 us -> 8 x 256 199 us; sigma = 1.25: 16 x 32 189 us ->
+    // 8 x 160 164 us; r02 tile sweep, tools/tile_sweep.sh)
+    const bool wide = cell_candidate && D == 2 && opt.batch >= 8;
     if (q == 0)
       q = D == 1 ? 512
-                 : (D == 2 ? ((cell_candidate && d == 1 && Nt[1] >= 512) ? 64
-                                                                         : ((cell_candidate && d == 0 && opt.batch >= 8) ? 16 : 32))
+                 : (D == 2 ? (wide ? (d == 0 ? 8 : (Nt[1] + (Nt[1] + 255) / 256 - 1) / ((Nt[1] + 255) / 256))
+                                   : ((cell_candidate && d == 1 && Nt[1] >= 512) ? 64 : 32))
                            : ((cell_candidate && d == 2) ? 16 : 8));
     q = std::min<int64_t>(q, Nt[d]);
     // cell-mode spreading reads a window of Q + 2m - 1 cells along the last dimension,
