@@ -725,7 +725,7 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
 }
 
 template <typename T>
-nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStream_t st) {
+nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStream_t st, bool overlap = false) {
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   auto* grid = (typename cplx<T>::type*)p->d_grid_adj;  // all zero on entry (plan creation / previous crop)
@@ -784,8 +784,9 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     // owner-computes segment gather (POLYNOMIAL or TENSOR taps): every grid cell written exactly once,
     // no zero pass
     rec(p, 1, 1);
+    // launch width: narrower when the direct NFFT runs concurrently (nfft_execute), resample1d.cuh
     const unsigned segs = std::min<unsigned>((unsigned)((p->Nt[0] + S1_SEG - 1) / S1_SEG),
-                                             (unsigned)(S1_CTAS_PER_SM * p->sm_count));
+                                             (unsigned)((overlap ? S1_CTAS_OVERLAP : S1_CTAS_ALONE) * p->sm_count));
     // FULL in 1D: the rows of B are the 2m taps, so the TENSOR kernel reads them
     CK(launch_k((p->tensor || p->full) ? ks.spread1t : ks.spread1, dim3(segs, (unsigned)p->B), S1_THREADS,
                 p->r1_spread_bytes, st, p->geom, WpnArg{p->wpn}, f, (const T*)p->d_kc,
@@ -981,7 +982,7 @@ nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, 
       f_in = p->d_stage_nodes2;
     }
     if (pre) CK(cudaStreamWaitEvent(p->side_adj, p->ev_pre, 0));
-    TRY(stage_spread<T>(p, (const C*)f_in, p->side_adj));
+    TRY(stage_spread<T>(p, (const C*)f_in, p->side_adj, fwd));
     TRY(stage_fft<T>(p, CUFFT_INVERSE, p->side_adj));
     TRY(stage_crop<T>(p, (C*)y_out, p->side_adj));
     if (h_y) CK(cudaMemcpyAsync(host_y, y_out, gbytes, cudaMemcpyDeviceToHost, p->side_adj));

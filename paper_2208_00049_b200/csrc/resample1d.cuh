@@ -156,10 +156,13 @@ constexpr int S1_THREADS = 128;
 constexpr int S1_K = 4;                   // consecutive cells per thread
 constexpr int S1_SEG = S1_THREADS * S1_K; // 512 cells per CTA
 constexpr int S1_CAP = 320;               // staged nodes per chunk (mean ~0.5 (SEG + 2m) at M = N = Nt/2)
-// resident CTAs per SM of the spread launch (grid-stride over the segments). Measured on B200 in the
-// bench step (direct || adjoint NFFT, 1D 2^18, m = 4): 4 per SM 45.3 us, 5: 46.0, 6: 46.4, one CTA per
-// segment (7 resident): 54.1 us -- a full grid of spread CTAs keeps the concurrent forward FFT off the SMs.
-constexpr int S1_CTAS_PER_SM = 4;
+// resident CTAs per SM of the spread launch (grid-stride over the segments, software-pipelined: the
+// next segment's loads overlap the current one's arithmetic). Measured on B200 (1D 2^18, m = 4): alone,
+// 4 per SM 10.5 us (3: 12.7, 2: 14.1); in the bench step with the direct NFFT running concurrently
+// (nfft_execute) the 121-register kernel at 4 per SM fills the register file and keeps the forward
+// FFT off the SMs (step 53.1 us), 3 per SM leaves it room (45.0 us). Hence two launch widths.
+constexpr int S1_CTAS_ALONE = 4;
+constexpr int S1_CTAS_OVERLAP = 3;
 
 // tap row pitch: 2m taps, odd pitch (neighbouring rows in distinct banks)
 __host__ __device__ constexpr int s1_pitch(int M) { return 2 * M + 1; }
@@ -182,6 +185,7 @@ __global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T
                                                               typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
   constexpr int TAPS = 2 * M, TP = s1_pitch(M), REACH = S1_K + 2 * M - 1;
+  constexpr int U = (S1_CAP + S1_THREADS - 1) / S1_THREADS;  // staged nodes per thread and chunk
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* sval = reinterpret_cast<C*>(smem_raw);
   T* stap = reinterpret_cast<T*>(sval + S1_CAP);
@@ -190,85 +194,86 @@ __global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T
   const int Nt = g.Nt[0], Mn = g.M;
   const int b = blockIdx.y;
   const int nsegs = (Nt + S1_SEG - 1) / S1_SEG;
-  // grid-stride over the segments (the launch may use fewer CTAs than segments)
-  for (int sgi = blockIdx.x; sgi < nsegs; sgi += gridDim.x) {
-  if (sgi != (int)blockIdx.x) __syncthreads();  // the previous segment's gathers are done
-  const int y0 = sgi * S1_SEG;
-  const int nseg = min(S1_SEG, Nt - y0);
-  const int W = nseg + 2 * M - 1;  // window cell u <-> binning cell y0 - m + u
-  // 1. virtual position of the first node of window cell u (u = W: one past the window's last node)
-  auto vpos = [&](int u) {
-    int c = y0 - M + u, wrap = 0;  // c in (-Nt, 2 Nt): 2m < Nt
-    if (c < 0) {
-      c += Nt;
-      wrap = -1;
-    } else if (c >= Nt) {
-      c -= Nt;
-      wrap = 1;
-    }
-    return __ldg(cstart + c) + wrap * Mn;
-  };
-  // the window's node range (uniform) and this thread's reach: window cells [K t, K t + REACH)
   const int t = threadIdx.x;
-  const int vbase = vpos(0), vend = vpos(W);
-  const int r_lo_v = vpos(min(S1_K * t, W)), r_hi_v = vpos(min(S1_K * t + REACH, W));
-  const int total = vend - vbase;
-  const int r_lo = r_lo_v - vbase, r_hi = r_hi_v - vbase;
-  C acc[S1_K];
-#pragma unroll
-  for (int k = 0; k < S1_K; ++k) {
-    acc[k].x = (T)0;
-    acc[k].y = (T)0;
-  }
   const C* fb = f + (long long)b * Mn;
-  NFFTB_TRACE(1);
-  for (int clo = 0; clo < total; clo += S1_CAP) {
-    const int cnt = min(S1_CAP, total - clo);
-    if (clo > 0) __syncthreads();  // previous chunk's gathers are done
-    // 2. stage the chunk: coordinates and indices, then the values' loads are issued and the taps
-    //    (which need only the coordinates) are evaluated while they are in flight
-    constexpr int U = (S1_CAP + S1_THREADS - 1) / S1_THREADS;
+  // 1. a segment's window: node range (virtual positions, uniform) and this thread's reach, window
+  //    cells [K t, K t + REACH); virtual position of window cell u: cstart[c mod Nt] + M floor(c / Nt)
+  struct Meta {
+    int y0, nseg, vbase, total, r_lo, r_hi;
+  };
+  auto load_meta = [&](int sgi) {
+    Meta mt;
+    mt.y0 = sgi * S1_SEG;
+    mt.nseg = min(S1_SEG, Nt - mt.y0);
+    const int W = mt.nseg + 2 * M - 1;  // window cell u <-> binning cell y0 - m + u
+    auto vpos = [&](int u) {
+      int c = mt.y0 - M + u, wrap = 0;  // c in (-Nt, 2 Nt): 2m < Nt
+      if (c < 0) {
+        c += Nt;
+        wrap = -1;
+      } else if (c >= Nt) {
+        c -= Nt;
+        wrap = 1;
+      }
+      return __ldg(cstart + c) + wrap * Mn;
+    };
+    mt.vbase = vpos(0);
+    mt.total = vpos(W) - mt.vbase;
+    mt.r_lo = vpos(min(S1_K * t, W)) - mt.vbase;
+    mt.r_hi = vpos(min(S1_K * t + REACH, W)) - mt.vbase;
+    return mt;
+  };
+  // 2. a chunk's nodes: coordinates and indices (first load level), then the values (second level)
+  struct Batch {
     int pp[U], jj[U], wv[U];
     double kk[U];
+    C v[U];
+  };
+  auto load_nodes = [&](const Meta& mt, int clo, Batch& bt) {
+    const int cnt = min(S1_CAP, mt.total - clo);
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int q = threadIdx.x + i * S1_THREADS;
-      pp[i] = -1;
-      jj[i] = -1;
-      wv[i] = 0;
-      kk[i] = 0.0;
+      const int q = t + i * S1_THREADS;
+      bt.pp[i] = -1;
+      bt.jj[i] = -1;
+      bt.wv[i] = 0;
+      bt.kk[i] = 0.0;
       if (q < cnt) {
-        int p = vbase + clo + q;  // virtual position in (-M, 2M)
+        int p = mt.vbase + clo + q;  // virtual position in (-M, 2M)
         if (p < 0) {
           p += Mn;
-          wv[i] = -1;
+          bt.wv[i] = -1;
         } else if (p >= Mn) {
           p -= Mn;
-          wv[i] = 1;
+          bt.wv[i] = 1;
         }
-        pp[i] = p;
-        kk[i] = (double)kc[p];
-        jj[i] = (p >= nb && p < ne) ? __ldg(jc + p) : -1;  // node shard = range [nb, ne) of the cell order
+        bt.pp[i] = p;
+        bt.kk[i] = (double)kc[p];
+        bt.jj[i] = (p >= nb && p < ne) ? __ldg(jc + p) : -1;  // node shard = range [nb, ne) of the cell order
       }
     }
-    C v[U];
+  };
+  auto load_vals = [&](Batch& bt) {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      v[i].x = (T)0;
-      v[i].y = (T)0;
-      if (jj[i] >= 0) v[i] = fb[jj[i]];
+      bt.v[i].x = (T)0;
+      bt.v[i].y = (T)0;
+      if (bt.jj[i] >= 0) bt.v[i] = fb[bt.jj[i]];
     }
+  };
+  // stage: taps (from the coordinates, or the TENSOR table), window cell and value of every node
+  auto stage = [&](const Meta& mt, const Batch& bt) {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int q = threadIdx.x + i * S1_THREADS;
-      if (pp[i] < 0) continue;
+      const int q = t + i * S1_THREADS;
+      if (bt.pp[i] < 0) continue;
       double frac;
-      const int c = node_cell(kk[i], g.Ntd[0], Nt, frac);
-      scel[q] = c + wv[i] * Nt - (y0 - M);  // window cell (virtual cell of the virtual position)
+      const int c = node_cell(bt.kk[i], g.Ntd[0], Nt, frac);
+      scel[q] = c + bt.wv[i] * Nt - (mt.y0 - M);  // window cell (virtual cell of the virtual position)
       T w[TAPS];
       if constexpr (TENSOR) {
 #pragma unroll
-        for (int l = 0; l < TAPS; ++l) w[l] = __ldg(wt + (long long)pp[i] * TAPS + l);
+        for (int l = 0; l < TAPS; ++l) w[l] = __ldg(wt + (long long)bt.pp[i] * TAPS + l);
       } else {
         window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
       }
@@ -278,42 +283,79 @@ __global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T
     }
 #pragma unroll
     for (int i = 0; i < U; ++i)
-      if (pp[i] >= 0) sval[threadIdx.x + i * S1_THREADS] = v[i];
-    NFFTB_TRACE(2);
-    __syncthreads();
-    NFFTB_TRACE(3);
-    // 3. owner-computes gather: node in window cell K t + v adds to cell K t + k with tap
-    //    l = k - v + 2m - 1 when 0 <= l < 2m
-    const int lo = max(r_lo - clo, 0), hi = min(r_hi - clo, cnt);
-    for (int q = lo; q < hi; ++q) {
-      const C val = sval[q];
-      const int l0 = TAPS - 1 - (scel[q] - S1_K * t);
-      const T* wr = stap + q * TP;
+      if (bt.pp[i] >= 0) sval[t + i * S1_THREADS] = bt.v[i];
+  };
+  int sgi = blockIdx.x;
+  if (sgi >= nsegs) return;
+  // software pipeline over this CTA's segments (grid-stride): the next segment's window bounds are
+  // loaded while the current one is staged, its nodes' coordinates / indices while it is gathered and
+  // their values right after, so its load chain overlaps the current segment's arithmetic
+  Meta mc = load_meta(sgi);
+  Batch bc, bn;
+  load_nodes(mc, 0, bc);
+  load_vals(bc);
+  NFFTB_TRACE(1);
+  while (true) {
+    const int sn = sgi + gridDim.x;
+    const bool has_next = sn < nsegs;
+    Meta mn;
+    if (has_next) mn = load_meta(sn);
+    C acc[S1_K];
 #pragma unroll
-      for (int k = 0; k < S1_K; ++k) {
-        const int l = l0 + k;
-        if ((unsigned)l < (unsigned)TAPS) {
-          const T wk = wr[l];
-          acc[k].x = fma(wk, val.x, acc[k].x);
-          acc[k].y = fma(wk, val.y, acc[k].y);
+    for (int k = 0; k < S1_K; ++k) {
+      acc[k].x = (T)0;
+      acc[k].y = (T)0;
+    }
+    for (int clo = 0; clo < mc.total; clo += S1_CAP) {
+      const int cnt = min(S1_CAP, mc.total - clo);
+      if (clo > 0) {  // a dense window: further chunks are loaded in place
+        __syncthreads();
+        load_nodes(mc, clo, bc);
+        load_vals(bc);
+      }
+      stage(mc, bc);
+      NFFTB_TRACE(2);
+      __syncthreads();
+      NFFTB_TRACE(3);
+      if (clo == 0 && has_next) load_nodes(mn, 0, bn);
+      // 3. owner-computes gather: node in window cell K t + v adds to cell K t + k with tap
+      //    l = k - v + 2m - 1 when 0 <= l < 2m
+      const int lo = max(mc.r_lo - clo, 0), hi = min(mc.r_hi - clo, cnt);
+      for (int q = lo; q < hi; ++q) {
+        const C val = sval[q];
+        const int l0 = TAPS - 1 - (scel[q] - S1_K * t);
+        const T* wr = stap + q * TP;
+#pragma unroll
+        for (int k = 0; k < S1_K; ++k) {
+          const int l = l0 + k;
+          if ((unsigned)l < (unsigned)TAPS) {
+            const T wk = wr[l];
+            acc[k].x = fma(wk, val.x, acc[k].x);
+            acc[k].y = fma(wk, val.y, acc[k].y);
+          }
         }
       }
     }
-  }
-  NFFTB_TRACE(4);
-  // 4. one plain store per owned cell (binning cell y <-> storage (y - Nt/2) mod Nt)
-  C* dst = grid + (long long)b * g.grid_cells;
-  int s = y0 + S1_K * t - (Nt >> 1);
-  if (s < 0) s += Nt;
+    if (has_next) load_vals(bn);
+    NFFTB_TRACE(4);
+    // 4. one plain store per owned cell (binning cell y <-> storage (y - Nt/2) mod Nt)
+    C* dst = grid + (long long)b * g.grid_cells;
+    int s = mc.y0 + S1_K * t - (Nt >> 1);
+    if (s < 0) s += Nt;
 #pragma unroll
-  for (int k = 0; k < S1_K; ++k) {
-    if (S1_K * t + k < nseg) {
-      int sk = s + k;
-      if (sk >= Nt) sk -= Nt;
-      dst[sk] = acc[k];
+    for (int k = 0; k < S1_K; ++k) {
+      if (S1_K * t + k < mc.nseg) {
+        int sk = s + k;
+        if (sk >= Nt) sk -= Nt;
+        dst[sk] = acc[k];
+      }
     }
+    if (!has_next) break;
+    __syncthreads();  // the gathers of this segment are done before the next one is staged
+    sgi = sn;
+    mc = mn;
+    bc = bn;
   }
-  }  // segments
 }
 
 // ---------------------------------------------------------------- TENSOR precompute (D = 1)

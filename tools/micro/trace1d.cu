@@ -90,7 +90,7 @@ static void run(int M_nodes, int Nt) {
   cudaMalloc(&flush, FL);
   const size_t sb = s1_smem_bytes(M, 16, 8), ib = i1_smem_bytes(M, 16);
   cudaFuncSetAttribute((const void*)spread1s_kernel<double, M, DEG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-  cudaFuncSetAttribute((const void*)interp1s_kernel<double, M, DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib);
+  cudaFuncSetAttribute((const void*)interp1s_kernel<double, M, DEG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib);
   const unsigned segs_s = std::min<unsigned>((Nt + S1_SEG - 1) / S1_SEG, g_s1cap ? g_s1cap * 148 : 1u << 30), segs_i = (Nt + I1_SEG - 1) / I1_SEG;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -113,7 +113,7 @@ static void run(int M_nodes, int Nt) {
                                                                                     M_nodes, d_grid);
     });
     const float ti = b2b([&] {
-      interp1s_kernel<double, M, DEG><<<dim3(segs_i, 1), I1_THREADS, ib, st>>>(g, wp, d_grid, d_kc, d_jc, d_cs, 0, M_nodes,
+      interp1s_kernel<double, M, DEG, false><<<dim3(segs_i, 1), I1_THREADS, ib, st>>>(g, wp, d_grid, d_kc, d_wt, d_jc, d_cs, 0, M_nodes,
                                                                                 d_out);
     });
     const float te = b2b([&] { empty_kernel<double><<<1024, 128, 0, st>>>(g, wpbig, d_out); });
@@ -155,7 +155,7 @@ static void run(int M_nodes, int Nt) {
         spread1s_kernel<double, M, DEG, false><<<dim3(segs_s, 1), S1_THREADS, sb>>>(g, wp, d_f, d_kc, d_wt, d_jc, d_cs, 0,
                                                                                    M_nodes, d_grid);
       else
-        interp1s_kernel<double, M, DEG><<<dim3(segs_i, 1), I1_THREADS, ib>>>(g, wp, d_grid, d_kc, d_jc, d_cs, 0, M_nodes,
+        interp1s_kernel<double, M, DEG, false><<<dim3(segs_i, 1), I1_THREADS, ib>>>(g, wp, d_grid, d_kc, d_wt, d_jc, d_cs, 0, M_nodes,
                                                                             d_out);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
