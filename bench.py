@@ -506,7 +506,8 @@ def run_steps(a, ctx, w, mode, steps, warmup, staged=False, with_pre=False, seq_
         torch.cuda.synchronize(ctx.dev)
     barrier(ctx)
     launches = launches_per_step * steps if g is not None else plan.launches() - l0
-    ms = sum(ev[s][0].elapsed_time(ev[s][1]) for s in range(steps))
+    per_step = [ev[s][0].elapsed_time(ev[s][1]) for s in range(steps)]
+    ms = sum(per_step)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=ctx.dev)
     if ctx.world > 1:
         import torch.distributed as dist
@@ -515,7 +516,7 @@ def run_steps(a, ctx, w, mode, steps, warmup, staged=False, with_pre=False, seq_
     features = sorted(plan.features())
     obj.close()
     return dict(ms=float(ms_t.item()), stage=stage, launches=launches, clocks=clk.summary(),
-                units_total=units_total, features=features)
+                units_total=units_total, features=features, median_ms=statistics.median(per_step))
 
 
 def roofline(w, means, step_ms, hbm, hbm_src, fp):
@@ -545,8 +546,9 @@ def roofline(w, means, step_ms, hbm, hbm_src, fp):
                  "algorithmic_bytes": bytes_of[dom], "algorithmic_flops": flops_of.get(dom, 0),
                  "kernel_ms_mean": means[dom], "kernel_share": means[dom] / step_ms,
                  "note": "kernel duration = marginal time of its stage in one graph of the seven stages run one "
-                         "after another (sequence time minus the sequence without the stage, L2 flushed before "
-                         "each; D >= 2 spread stage includes the value permutation kernel)"})
+                         "after another (median sequence time minus the median of the sequence without the stage, "
+                         "L2 flushed before each step; D >= 2 spread stage includes the value permutation "
+                         "kernel)"})
     return roof
 
 
@@ -568,11 +570,13 @@ def measure_config(a, ctx, config, mode, steps, warmup, m=None, e2e=True, cpu=Tr
         means = {k: (statistics.mean(v) if v else 0.0) for k, v in st["stage"].items()}
         out["stages_ms_mean"] = means
         out["ms_per_step_sequential"] = st["ms"] / n2
-        # marginal stage times: the seven-stage sequence with and without each stage (no event nodes)
-        full = run_steps(a, ctx, w, mode, n2, warmup, seq_omit=-1)["ms"] / n2
+        # marginal stage times: the seven-stage sequence with and without each stage (no event nodes);
+        # medians of the per-step times (the flush before every step makes single steps noisy)
+        n3 = max(n2, 60)
+        full = run_steps(a, ctx, w, mode, n3, warmup, seq_omit=-1)["median_ms"]
         marg = {}
         for k, name in enumerate(["precompute", "deconv", "fft_fwd", "interp", "spread", "fft_adj", "crop"]):
-            marg[name] = full - run_steps(a, ctx, w, mode, n2, warmup, seq_omit=k)["ms"] / n2
+            marg[name] = full - run_steps(a, ctx, w, mode, n3, warmup, seq_omit=k)["median_ms"]
         out["stages_ms_marginal"] = marg
         out["ms_per_step_sequential_no_events"] = full
         if with_pre:

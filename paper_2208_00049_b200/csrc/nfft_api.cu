@@ -232,6 +232,24 @@ cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStr
   void* args[] = {arg_ptr(a)...};
   return cudaLaunchKernel(fn, grid, block, args, smem, st);
 }
+// The same with programmatic dependent launch: the kernel may start before the previous kernel on the
+// stream has finished and waits (griddepcontrol.wait) before it reads that kernel's output, so its
+// independent prologue (node loads) and launch overlap the previous kernel's tail (the FFT).
+template <typename... A>
+cudaError_t launch_k_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... a) {
+  void* args[] = {arg_ptr(a)...};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
 
 template <typename T>
 nfft_status build_window_tables(nfft_plan p) {
@@ -687,8 +705,11 @@ nfft_status stage_fft(nfft_plan p, int dir, cudaStream_t st) {
   return r == CUFFT_SUCCESS ? NFFT_SUCCESS : NFFT_ERROR_CUFFT;
 }
 
+// pdl: the kernel right before on `st` is this plan's forward FFT (nfft_forward, nfft_execute without a
+// concurrent precompute), so the interpolation may launch programmatically: its node loads overlap the
+// FFT's tail and it waits for the grid (griddepcontrol.wait) before staging it
 template <typename T>
-nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st) {
+nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st, bool pdl = false) {
   const KernelSet<T>& ks = kernels_of<T>(p);
   const WinPoly<T>& wp = poly_of<T>(p);
   (void)wp;
@@ -701,7 +722,10 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
     CK(launch_k(ks.full_interp, dim3(ctas, (unsigned)p->B), FI_THREADS, 0, st, p->geom, grid, (const T*)p->d_bw,
                 (const int*)p->d_bi, (const int*)p->d_jc, p->node_begin, p->node_end, f));
   } else if (p->cellmode && p->D >= 2) {
-    CK(launch_k(p->tensor ? ks.interp_cellt : ks.interp_cell, dim3((unsigned)p->n_tiles, (unsigned)p->B), RC_THREADS,
+    CK((pdl ? launch_k_pdl<Geom, WpnArg, const typename cplx<T>::type*, const T*, const T*, const int*, const int*, int,
+                           int, typename cplx<T>::type*>
+            : launch_k<Geom, WpnArg, const typename cplx<T>::type*, const T*, const T*, const int*, const int*, int, int,
+                       typename cplx<T>::type*>)(p->tensor ? ks.interp_cellt : ks.interp_cell, dim3((unsigned)p->n_tiles, (unsigned)p->B), RC_THREADS,
                 p->region_bytes, st, p->geom, wpn, grid, (const T*)p->d_kc, (const T*)p->d_wt, (const int*)p->d_jc,
                 (const int*)p->d_cstart, p->node_begin, p->node_end, f));
   } else if (p->use_ind) {
@@ -709,7 +733,10 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
         p->geom, wp, grid, (const T*)p->d_ks, p->d_perm, p->d_offsets, p->node_begin, p->node_end, f);
   } else if (p->cellmode && p->D == 1) {
     const unsigned segs = (unsigned)((p->Nt[0] + I1_SEG - 1) / I1_SEG);
-    CK(launch_k(p->tensor ? ks.interp1t : ks.interp1, dim3(segs, (unsigned)p->B), I1_THREADS, p->r1_interp_bytes, st,
+    CK((pdl ? launch_k_pdl<Geom, WpnArg, const typename cplx<T>::type*, const T*, const T*, const int*, const int*, int,
+                           int, typename cplx<T>::type*>
+            : launch_k<Geom, WpnArg, const typename cplx<T>::type*, const T*, const T*, const int*, const int*, int, int,
+                       typename cplx<T>::type*>)(p->tensor ? ks.interp1t : ks.interp1, dim3(segs, (unsigned)p->B), I1_THREADS, p->r1_interp_bytes, st,
                 p->geom, wpn, grid, (const T*)p->d_kc, (const T*)p->d_wt, (const int*)p->d_jc, (const int*)p->d_cstart,
                 p->node_begin, p->node_end, f));
   } else if (p->tiled) {
@@ -880,7 +907,7 @@ nfft_status forward_impl(nfft_plan p, const void* fhat_in, void* f_out) {
   rec(p, 0, 1);
   TRY(stage_fft<T>(p, CUFFT_FORWARD, p->stream));
   rec(p, 0, 2);
-  TRY(stage_interp<T>(p, f, p->stream));
+  TRY(stage_interp<T>(p, f, p->stream, true));
   rec(p, 0, 3);
   if (host_out) {
     CK(cudaMemcpyAsync(f_out, f, node_bytes, cudaMemcpyDeviceToHost, p->stream));
@@ -996,7 +1023,7 @@ nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, 
     TRY(stage_deconv<T>(p, (const C*)fhat, p->stream));
     TRY(stage_fft<T>(p, CUFFT_FORWARD, p->stream));
     if (pre) CK(cudaStreamWaitEvent(p->stream, p->ev_pre, 0));
-    TRY(stage_interp<T>(p, (C*)f_out, p->stream));
+    TRY(stage_interp<T>(p, (C*)f_out, p->stream, !pre));
     if (h_fout) CK(cudaMemcpyAsync(host_fout, f_out, nbytes, cudaMemcpyDeviceToHost, p->stream));
   }
   if (pre) CK(cudaStreamWaitEvent(p->stream, p->ev_pre, 0));

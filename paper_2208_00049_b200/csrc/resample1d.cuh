@@ -67,20 +67,8 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
   const int y0 = sgi * I1_SEG;
   const int nseg = min(I1_SEG, Nt - y0);
   const int W = nseg + TAPS - 1;
-  // 1. the block index set -> shared memory (asynchronous; storage (cell - Nt/2) mod Nt)
-  {
-    const C* gb = grid + (long long)b * g.grid_cells;
-    int s0 = y0 - M + 1 - (Nt >> 1);
-    if (s0 < 0) s0 += Nt;
-    if (s0 < 0) s0 = pos_mod(s0, Nt);
-    for (int e = threadIdx.x; e < W; e += I1_THREADS) {
-      int s = s0 + e;
-      while (s >= Nt) s -= Nt;
-      cp_async_cell<T>(sg + e, gb + s);
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
-  // 2. this CTA's nodes (cell-sorted range of its cells), clipped to the shard [nb, ne)
+  // 1. this CTA's nodes (cell-sorted range of its cells), clipped to the shard [nb, ne): they do not
+  //    depend on the grid, so with programmatic dependent launch they load while the FFT finishes
   const int p0 = max(__ldg(cstart + y0), nb), p1 = min(__ldg(cstart + y0 + nseg), ne);
   double kk[I1_U];
   int jj[I1_U];
@@ -93,6 +81,20 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
       kk[i] = (double)kc[p];
       jj[i] = jc[p];
     }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the grid (previous kernel's output) is complete
+  // 2. the block index set -> shared memory (asynchronous; storage (cell - Nt/2) mod Nt)
+  {
+    const C* gb = grid + (long long)b * g.grid_cells;
+    int s0 = y0 - M + 1 - (Nt >> 1);
+    if (s0 < 0) s0 += Nt;
+    if (s0 < 0) s0 = pos_mod(s0, Nt);
+    for (int e = threadIdx.x; e < W; e += I1_THREADS) {
+      int s = s0 + e;
+      while (s >= Nt) s -= Nt;
+      cp_async_cell<T>(sg + e, gb + s);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();

@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel
     }
   };
   const int b = blockIdx.y;  // batch vector of this CTA (config 5: B = 32 CTAs per tile)
-  stage(grid + (long long)b * g.grid_cells);
-  // the tile's nodes: one cell-sorted range per tile row (all but the last dimension)
+  // the tile's nodes: one cell-sorted range per tile row (all but the last dimension); independent of
+  // the grid, so under programmatic dependent launch this overlaps the FFT's tail
   const int nrows = D == 2 ? Qt[0] : Qt[0] * Qt[1];
   {
     const int per = (nrows + RC_THREADS - 1) / RC_THREADS;
@@ -142,6 +142,8 @@ __global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel
     if (threadIdx.x == 0) rpre[nrows] = tot;
   }
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the grid (previous kernel's output) is complete
+  stage(grid + (long long)b * g.grid_cells);
   const int total = rpre[nrows];
   auto position = [&](int q) {  // q-th node of the tile -> cell-sorted position (binary search over rows)
     int lo = 0, hi = nrows;
