@@ -776,8 +776,9 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     transpose_bm_kernel<T><<<dim3((unsigned)((p->M + 31) / 32), nch), 256, 0, st>>>(f, (int)p->B, (int)p->M, p->bp,
                                                                                    p->d_inv, (C*)p->d_fT);
     const unsigned segs = (unsigned)(p->Nt[0] * ((p->Nt[1] + RB_SEG - 1) / RB_SEG));
-    ks.spread_rowbatch<<<dim3(segs, nch), RB_THREADS, p->rb_bytes, st>>>(p->geom, (const C*)p->d_fT, p->bp,
-                                                                         (const T*)p->d_wt, p->d_cstart, grid);
+    // programmatic dependent launch: the rows' cstart loads overlap transpose_bm's tail
+    CK(launch_k_pdl((const void*)ks.spread_rowbatch, dim3(segs, nch), RB_THREADS, p->rb_bytes, st, p->geom,
+                    (const C*)p->d_fT, p->bp, (const T*)p->d_wt, (const int*)p->d_cstart, grid));
     p->launches += 2;
     CKL();
     return NFFT_SUCCESS;
@@ -792,8 +793,10 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     long long nblk = (p->Nt[0] + WB_K0 - 1) / WB_K0;
     if (p->D == 3) nblk *= (p->Nt[1] + 3) / 4 * ((p->Nt[2] + 7) / 8);
     else nblk *= (p->Nt[1] + 31) / 32;
-    ks.spread_wb<<<dim3((unsigned)((nblk + WB_WARPS - 1) / WB_WARPS), (unsigned)p->B), 32 * WB_WARPS, p->wb_bytes, st>>>(
-        p->geom, (const C*)p->d_fc, p->d_cl, (const T*)p->d_wt, p->d_cstart, grid);
+    // programmatic dependent launch: the warps' window enumeration overlaps permute_f's tail
+    CK(launch_k_pdl((const void*)ks.spread_wb, dim3((unsigned)((nblk + WB_WARPS - 1) / WB_WARPS), (unsigned)p->B),
+                    32 * WB_WARPS, p->wb_bytes, st, p->geom, (const C*)p->d_fc, (const int*)p->d_cl, (const T*)p->d_wt,
+                    (const int*)p->d_cstart, grid));
     p->launches += 2;
     CKL();
     return NFFT_SUCCESS;

@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(RB_THREADS) spread_rowbatch_kernel(
       lo_l = __ldg(cstart + rowkey + col);
       hi_l = __ldg(cstart + rowkey + col + 1);
     }
+    if (r == warp) asm volatile("griddepcontrol.wait;" ::: "memory");  // f^T comes from transpose_bm
     rb_row<T, M>(lo_l, hi_l, TAPS - 1 - r, fTc, BP, wt, acc);
   }
   // sum the warps' partial rows (row pitch 33 vectors: conflict-free), coalesced stores (consecutive

@@ -249,6 +249,9 @@ __global__ void __launch_bounds__(32 * WB_WARPS) spread_wb_kernel(Geom g, const 
     acc[k].y = (T)0;
   }
   int slot = 0;
+  // the values in cell order come from the previous kernel (permute_f): under programmatic dependent
+  // launch the window enumeration above overlaps its tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (u0 < Cfg::W0) stage(0, u0, q0);
   while (u0 < Cfg::W0) {
     // next batch: rest of this plane, else the next non-empty plane
