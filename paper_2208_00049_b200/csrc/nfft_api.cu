@@ -453,7 +453,7 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
       int o = 0;
       ok = cudaFuncSetAttribute((const void*)ks.spread_rowbatch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)p->rb_bytes) == cudaSuccess &&
-           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void*)ks.spread_rowbatch, RB_THREADS, p->rb_bytes) ==
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void*)ks.spread_rowbatch, rb_threads(p->m), p->rb_bytes) ==
                cudaSuccess &&
            o >= 1;
       cudaGetLastError();
@@ -775,9 +775,9 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     const unsigned nch = (unsigned)(p->bp / RB_LANES);
     transpose_bm_kernel<T><<<dim3((unsigned)((p->M + 31) / 32), nch), 256, 0, st>>>(f, (int)p->B, (int)p->M, p->bp,
                                                                                    p->d_inv, (C*)p->d_fT);
-    const unsigned segs = (unsigned)(p->Nt[0] * ((p->Nt[1] + RB_SEG - 1) / RB_SEG));
+    const unsigned segs = (unsigned)(((p->Nt[0] + RB_ROWS - 1) / RB_ROWS) * ((p->Nt[1] + RB_SEG - 1) / RB_SEG));
     // programmatic dependent launch: the rows' cstart loads overlap transpose_bm's tail
-    CK(launch_k_pdl((const void*)ks.spread_rowbatch, dim3(segs, nch), RB_THREADS, p->rb_bytes, st, p->geom,
+    CK(launch_k_pdl((const void*)ks.spread_rowbatch, dim3(segs, nch), rb_threads(p->m), p->rb_bytes, st, p->geom,
                     (const C*)p->d_fT, p->bp, (const T*)p->d_wt, (const int*)p->d_cstart, grid));
     p->launches += 2;
     CKL();

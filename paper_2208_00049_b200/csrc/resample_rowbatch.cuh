@@ -30,11 +30,12 @@
 
 namespace nfftb {
 
-#ifndef RB_NWARPS
-#define RB_NWARPS 8
-#endif
-constexpr int RB_THREADS = 32 * RB_NWARPS;  // warps per CTA (the 2m window rows are dealt round-robin)
+
 constexpr int RB_LANES = 32;     // vectors per chunk
+// consecutive grid rows per CTA (a window row's node visit then serves all of them). Measured on the
+// radial configs (sigma 2 / 1.25): 1 row 423 / 496 us, 2 rows (2m + 1 warps) 476 / 535 us (110
+// registers; the extra FMAs per visit do not pay for the lower occupancy)
+constexpr int RB_ROWS = 1;
 constexpr int RB_SEG = 16;       // cells per CTA (last dimension)
 constexpr int RB_PITCH = 33;     // partial-row pitch in shared memory (vectors + 1)
 
@@ -95,8 +96,7 @@ __global__ void __launch_bounds__(256) transpose_mb_kernel(const typename cplx<T
 }
 
 __host__ __device__ inline size_t rb_smem_bytes(int M, int rsize) {
-  (void)M;
-  return (size_t)(RB_THREADS / 32) * RB_SEG * RB_PITCH * 2 * rsize;  // per-warp partial rows
+  return (size_t)(2 * M + RB_ROWS - 1) * RB_SEG * RB_PITCH * 2 * rsize;  // per-warp partial rows
 }
 
 // Taps of every cell-sorted node, wt[pos][d][t] (the paper's TENSOR layout,
@@ -136,10 +136,15 @@ __global__ void __launch_bounds__(TN_NODES) taps_nd_kernel(Geom g, WinPolyN<T, D
 
 // Visits of the nodes [lo, hi) of window column U (compile-time) of one window
 // row: cell k of the segment gets tap k - U + 2m - 1 of the last dimension, so
-// only the cells in the node's reach are accumulated (no zero products).
+// only the cells in the node's reach are accumulated (no zero products along
+// the last dimension). The CTA owns RB_ROWS consecutive grid rows: output row
+// j takes the node's dimension-0 tap lead + j (zero where lead + j is outside
+// [0, 2m): the first and last window rows reach one output row only), so the
+// node's value, taps and address arithmetic serve RB_ROWS rows.
 template <typename T, int M, int U>
 __device__ __forceinline__ void rb_visit(int lo, int hi, int lead, const typename cplx<T>::type* __restrict__ fTc,
-                                         int BP, const T* __restrict__ wt, typename cplx<T>::type (&acc)[RB_SEG]) {
+                                         int BP, const T* __restrict__ wt,
+                                         typename cplx<T>::type (&acc)[RB_ROWS][RB_SEG]) {
   using C = typename cplx<T>::type;
   constexpr int TAPS = 2 * M;
   constexpr int KLO = U - TAPS + 1 > 0 ? U - TAPS + 1 : 0;
@@ -149,7 +154,9 @@ __device__ __forceinline__ void rb_visit(int lo, int hi, int lead, const typenam
   for (int pos = lo; pos < hi; ++pos) {
     const C v = fTc[(long long)pos * BP];
     const T* wp = wt + (long long)pos * 2 * TAPS;
-    const T w0 = __ldg(wp + lead);
+    T w0[RB_ROWS];
+#pragma unroll
+    for (int j = 0; j < RB_ROWS; ++j) w0[j] = (unsigned)(lead + j) < (unsigned)TAPS ? __ldg(wp + lead + j) : (T)0;
     T w1[TAPS];
     if constexpr (VEC && sizeof(T) == 4) {
 #pragma unroll
@@ -167,19 +174,22 @@ __device__ __forceinline__ void rb_visit(int lo, int hi, int lead, const typenam
 #pragma unroll
       for (int t = 0; t < TAPS; ++t) w1[t] = __ldg(wp + TAPS + t);
     }
-    const T vx = w0 * v.x, vy = w0 * v.y;
 #pragma unroll
-    for (int k = KLO; k <= KHI; ++k) {
-      const T w = w1[k - U + TAPS - 1];
-      acc[k].x = fma(w, vx, acc[k].x);
-      acc[k].y = fma(w, vy, acc[k].y);
+    for (int j = 0; j < RB_ROWS; ++j) {
+      const T vx = w0[j] * v.x, vy = w0[j] * v.y;
+#pragma unroll
+      for (int k = KLO; k <= KHI; ++k) {
+        const T w = w1[k - U + TAPS - 1];
+        acc[j][k].x = fma(w, vx, acc[j][k].x);
+        acc[j][k].y = fma(w, vy, acc[j][k].y);
+      }
     }
   }
 }
 
 template <typename T, int M, int U = 0>
 __device__ __forceinline__ void rb_row(int lo_l, int hi_l, int lead, const typename cplx<T>::type* fTc, int BP,
-                                       const T* wt, typename cplx<T>::type (&acc)[RB_SEG]) {
+                                       const T* wt, typename cplx<T>::type (&acc)[RB_ROWS][RB_SEG]) {
   if constexpr (U < RB_SEG + 2 * M - 1) {
     const int lo = __shfl_sync(0xffffffffu, lo_l, U), hi = __shfl_sync(0xffffffffu, hi_l, U);
     if (lo < hi) rb_visit<T, M, U>(lo, hi, lead, fTc, BP, wt, acc);
@@ -187,35 +197,44 @@ __device__ __forceinline__ void rb_row(int lo_l, int hi_l, int lead, const typen
   }
 }
 
-// One CTA owns SEG cells of one grid row for 32 vectors; warp w walks window rows
-// w, w + 8, ... (lead tap 2m - 1 - r), each window column's nodes in cell order
-// (per-cell ranges from cstart, lane u holds column u's), then the warps'
-// partial rows are summed in shared memory and stored coalesced.
+// One CTA owns SEG cells of RB_ROWS consecutive grid rows for 32 vectors; warp w
+// walks window rows w, w + 8, ... of the 2m + RB_ROWS - 1 in reach (lead tap
+// 2m - 1 - r for the first output row), each window column's nodes in cell
+// order (per-cell ranges from cstart, lane u holds column u's), then the warps'
+// partial rows are summed in shared memory, one output row at a time, and
+// stored coalesced.
+// one warp per window row
+__host__ __device__ constexpr int rb_threads(int M) { return 32 * (2 * M + RB_ROWS - 1); }
+
 template <typename T, int M>
-__global__ void __launch_bounds__(RB_THREADS) spread_rowbatch_kernel(
+__global__ void __launch_bounds__(rb_threads(M)) spread_rowbatch_kernel(
     Geom g, const typename cplx<T>::type* __restrict__ fTc, int BP, const T* __restrict__ wt,
     const int* __restrict__ cstart, typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
   constexpr int TAPS = 2 * M;
-  constexpr int NW = RB_THREADS / 32;
-  constexpr int WC = RB_SEG + TAPS - 1;  // window columns
+  constexpr int NW = rb_threads(M) / 32;
+  constexpr int WR = TAPS + RB_ROWS - 1;  // window rows
+  constexpr int WC = RB_SEG + TAPS - 1;   // window columns
   static_assert(WC <= 32, "window columns per lane");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b0 = blockIdx.y * RB_LANES;
   const int Nt0 = g.Nt[0], NtL = g.Nt[1];
   const int nseg = (NtL + RB_SEG - 1) / RB_SEG;
-  const int y0 = blockIdx.x / nseg, c0 = (blockIdx.x - y0 * nseg) * RB_SEG;  // binning row, first column
+  const int rb = blockIdx.x / nseg;
+  const int y0 = rb * RB_ROWS, c0 = (blockIdx.x - rb * nseg) * RB_SEG;  // first binning row, first column
   const int qs = min(RB_SEG, NtL - c0);
   C* part = reinterpret_cast<C*>(smem_raw);  // [NW][SEG][RB_PITCH]
-  C acc[RB_SEG];
+  C acc[RB_ROWS][RB_SEG];
 #pragma unroll
-  for (int k = 0; k < RB_SEG; ++k) {
-    acc[k].x = (T)0;
-    acc[k].y = (T)0;
-  }
+  for (int j = 0; j < RB_ROWS; ++j)
+#pragma unroll
+    for (int k = 0; k < RB_SEG; ++k) {
+      acc[j][k].x = (T)0;
+      acc[j][k].y = (T)0;
+    }
   fTc += b0 + lane;
-  for (int r = warp; r < TAPS; r += NW) {  // window row x0 = y0 - m + r
+  for (int r = warp; r < WR; r += NW) {  // window row x0 = y0 - m + r
     int xr = y0 - M + r;  // in (-Nt0, 2 Nt0): one conditional wrap
     if (xr < 0) xr += Nt0;
     else if (xr >= Nt0) xr -= Nt0;
@@ -231,32 +250,36 @@ __global__ void __launch_bounds__(RB_THREADS) spread_rowbatch_kernel(
     if (r == warp) asm volatile("griddepcontrol.wait;" ::: "memory");  // f^T comes from transpose_bm
     rb_row<T, M>(lo_l, hi_l, TAPS - 1 - r, fTc, BP, wt, acc);
   }
-  // sum the warps' partial rows (row pitch 33 vectors: conflict-free), coalesced stores (consecutive
-  // threads = consecutive cells of a vector)
-#pragma unroll
-  for (int k = 0; k < RB_SEG; ++k) part[((size_t)warp * RB_SEG + k) * RB_PITCH + lane] = acc[k];
-  __syncthreads();
+  // sum the warps' partial rows (row pitch 33 vectors: conflict-free), one output row at a time,
+  // coalesced stores (consecutive threads = consecutive cells of a vector)
   const int nbc = min(RB_LANES, g.B - b0);
-  int ys = y0 - (Nt0 >> 1);
-  if (ys < 0) ys += Nt0;
-  const long long rowoff = (long long)ys * NtL;
   int cs0 = c0 - (NtL >> 1);
   if (cs0 < 0) cs0 += NtL;
-  for (int idx = tid; idx < nbc * RB_SEG; idx += RB_THREADS) {
-    const int bb = idx / RB_SEG, k = idx - bb * RB_SEG;
-    if (k >= qs) continue;
-    C a;
-    a.x = (T)0;
-    a.y = (T)0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const C c = part[((size_t)w * RB_SEG + k) * RB_PITCH + bb];
-      a.x += c.x;
-      a.y += c.y;
+  for (int j = 0; j < RB_ROWS; ++j) {
+    if (j > 0) __syncthreads();  // the previous row's partials are consumed
+#pragma unroll
+    for (int k = 0; k < RB_SEG; ++k) part[((size_t)warp * RB_SEG + k) * RB_PITCH + lane] = acc[j][k];
+    __syncthreads();
+    int ys = y0 + j - (Nt0 >> 1);
+    if (ys < 0) ys += Nt0;
+    const long long rowoff = (long long)ys * NtL;
+    for (int idx = tid; idx < nbc * RB_SEG; idx += NW * 32) {
+      const int bb = idx / RB_SEG, k = idx - bb * RB_SEG;
+      if (k >= qs) continue;
+      C a;
+      a.x = (T)0;
+      a.y = (T)0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const C c = part[((size_t)w * RB_SEG + k) * RB_PITCH + bb];
+        a.x += c.x;
+        a.y += c.y;
+      }
+      int cs = cs0 + k;
+      if (cs >= NtL) cs -= NtL;
+      grid[(long long)(b0 + bb) * g.grid_cells + rowoff + cs] = a;
     }
-    int cs = cs0 + k;
-    if (cs >= NtL) cs -= NtL;
-    grid[(long long)(b0 + bb) * g.grid_cells + rowoff + cs] = a;
   }
 }
 
