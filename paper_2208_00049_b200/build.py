@@ -47,7 +47,13 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in _deps())
 
 
-def build(force=False, jobs=None, verbose=True):
+def build(force=False, jobs=None, verbose=True, defines=(), out=None):
+    """defines / out: experiment builds (extra -D flags into their own object
+    directory and library file); the product library takes neither."""
+    global OBJ, LIB
+    if defines or out:
+        tag = "_".join(d.replace("=", "") for d in defines) or "x"
+        OBJ, LIB = os.path.join(ROOT, "build", "obj_" + tag), out or os.path.join(HERE, f"libnfft_b200_{tag}.so")
     if not force and up_to_date():
         if verbose:
             print(f"[build] {LIB} up to date")
@@ -66,7 +72,7 @@ def build(force=False, jobs=None, verbose=True):
                 files = [f for f in fh.read().replace("\\\n", " ").split()[1:] if os.path.exists(f)]
             if files and all(os.path.getmtime(f) <= os.path.getmtime(obj) for f in files):
                 return obj
-        cmd = [nv] + ARCH + FLAGS + ["-c", src, "-o", obj, "-MD", "-MF", dep]
+        cmd = [nv] + ARCH + FLAGS + ["-D" + d for d in defines] + ["-c", src, "-o", obj, "-MD", "-MF", dep]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
@@ -90,6 +96,8 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=None)
+    ap.add_argument("-D", action="append", default=[], help="experiment build: extra define")
+    ap.add_argument("--out", default=None, help="experiment build: library path")
     a = ap.parse_args()
-    build(force=a.force, jobs=a.j)
+    build(force=a.force, jobs=a.j, defines=a.D, out=a.out)
     sys.exit(0)

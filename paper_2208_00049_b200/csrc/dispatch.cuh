@@ -38,6 +38,8 @@ struct KernelSet {
   const void* spread_cell;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 2 batches: row-segment spread, lanes = batch vectors (resample_rowbatch.cuh)
   void (*spread_rowbatch)(Geom, const C*, int, const T*, const int*, C*);
+  // second generation: parts split evenly over the warps, cp.async-staged chunks, FFMA2
+  void (*spread_rb2)(Geom, const C*, int, const T*, const int*, const int*, C*);
   const void* taps_nd;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 2, 3: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
   void (*spread_wb)(Geom, const C*, const int*, const T*, const int*, C*);
@@ -99,7 +101,10 @@ KernelSet<T> make_set() {
     k.interp_cellt = (const void*)interp_cell_kernel<T, D, M, DEG, true>;
     k.full_spread = (const void*)full_spread_kernel<T, D, M>;
     k.spread_cell = (const void*)spread_cell_kernel<T, D, M, DEG>;
-    if constexpr (D == 2) k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
+    if constexpr (D == 2) {
+      k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
+      k.spread_rb2 = spread_rb2_kernel<T, M>;
+    }
     k.taps_nd = (const void*)taps_nd_kernel<T, D, M, DEG>;
     k.spread_wb = spread_wb_kernel<T, D, M>;
     k.wb_warp_bytes = WbCfg<T, D, M>::WARP_BYTES;

@@ -447,13 +447,13 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     if (!ok) p->tensor = p->full = false;
   }
   if (p->batchmode) {
-    bool ok = p->cellmode && ks.spread_rowbatch;
+    bool ok = p->cellmode && ks.spread_rb2;
     if (ok) {
-      p->rb_bytes = rb_smem_bytes(p->m, (int)p->rsize());
+      p->rb_bytes = rb2_smem_bytes(p->m, (int)p->rsize());
       int o = 0;
-      ok = cudaFuncSetAttribute((const void*)ks.spread_rowbatch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      ok = cudaFuncSetAttribute((const void*)ks.spread_rb2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)p->rb_bytes) == cudaSuccess &&
-           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void*)ks.spread_rowbatch, rb_threads(p->m), p->rb_bytes) ==
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void*)ks.spread_rb2, 32 * RB2_WARPS, p->rb_bytes) ==
                cudaSuccess &&
            o >= 1;
       cudaGetLastError();
@@ -635,7 +635,7 @@ nfft_status precompute_impl(nfft_plan p, cudaStream_t st) {
       // taps of every node for the D >= 2 adjoint / the TENSOR strategy (layout wt[pos][d][t])
       const KernelSet<R>& ks = kernels_of<R>(p);
       CK(launch_k(ks.taps_nd, (unsigned)((p->M + TN_NODES - 1) / TN_NODES), TN_NODES, 0, st, p->geom, WpnArg{p->wpn},
-                  (const R*)p->d_kc, (R*)p->d_wt, p->wbmode ? p->d_cl : (int*)nullptr));
+                  (const R*)p->d_kc, (R*)p->d_wt, (p->wbmode || p->batchmode) ? p->d_cl : (int*)nullptr));
       ++p->launches;
       if (p->batchmode) {
         invert_perm_kernel<<<(unsigned)((p->M + 255) / 256), 256, 0, st>>>(p->d_jc, (int)p->M, p->d_inv);
@@ -775,10 +775,11 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     const unsigned nch = (unsigned)(p->bp / RB_LANES);
     transpose_bm_kernel<T><<<dim3((unsigned)((p->M + 31) / 32), nch), 256, 0, st>>>(f, (int)p->B, (int)p->M, p->bp,
                                                                                    p->d_inv, (C*)p->d_fT);
-    const unsigned segs = (unsigned)(((p->Nt[0] + RB_ROWS - 1) / RB_ROWS) * ((p->Nt[1] + RB_SEG - 1) / RB_SEG));
-    // programmatic dependent launch: the rows' cstart loads overlap transpose_bm's tail
-    CK(launch_k_pdl((const void*)ks.spread_rowbatch, dim3(segs, nch), rb_threads(p->m), p->rb_bytes, st, p->geom,
-                    (const C*)p->d_fT, p->bp, (const T*)p->d_wt, (const int*)p->d_cstart, grid));
+    const int S = Rb2Cfg<T>::S, R = Rb2Cfg<T>::R;
+    const unsigned segs = (unsigned)((p->Nt[0] + R - 1) / R * ((p->Nt[1] + S - 1) / S));
+    // programmatic dependent launch: the parts' cstart loads overlap transpose_bm's tail
+    CK(launch_k_pdl((const void*)ks.spread_rb2, dim3(segs, nch), 32 * RB2_WARPS, p->rb_bytes, st, p->geom,
+                    (const C*)p->d_fT, p->bp, (const T*)p->d_wt, (const int*)p->d_cl, (const int*)p->d_cstart, grid));
     p->launches += 2;
     CKL();
     return NFFT_SUCCESS;
@@ -1274,11 +1275,13 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
   // 2D batches of >= 8 transforms: row-segment adjoint with lanes = batch vectors (not for node
   // shards; the 16 + 2m - 1 window columns must not wrap onto themselves)
   p->batchmode = p->cellmode && !p->full && D == 2 && p->B >= 8 && opt.node_begin == 0 &&
-                 (opt.node_end == 0 || opt.node_end == M) && Nt[1] >= RB_SEG + 2 * m - 1;
+                 (opt.node_end == 0 || opt.node_end == M) &&
+                 Nt[1] >= (c128 ? Rb2Cfg<double>::S : Rb2Cfg<float>::S) + 2 * m - 1 &&
+                 Nt[0] >= (c128 ? Rb2Cfg<double>::R : Rb2Cfg<float>::R) + 2 * m - 1;
   p->bp = (int)((p->B + 31) / 32 * 32);
   if (ok && p->batchmode)
     ok = alloc(&p->d_fT, (size_t)M * p->bp * csz) && (p->d_wt || alloc(&p->d_wt, (size_t)M * D * 2 * m * rs)) &&
-         alloc((void**)&p->d_inv, (size_t)M * 4);
+         alloc((void**)&p->d_inv, (size_t)M * 4) && (p->d_cl || alloc((void**)&p->d_cl, (size_t)M * 4));
   // D = 2, 3 (not batched): warp-block adjoint over the TENSOR taps; the last-dimension window
   // (32 or 8 lanes + 2m - 1 cells) must not wrap onto itself
   p->wbmode = p->cellmode && !p->full && !p->batchmode && D >= 2 && Nt[D - 1] >= (D == 3 ? 8 : 32) + 2 * m - 1;

@@ -283,4 +283,349 @@ __global__ void __launch_bounds__(rb_threads(M)) spread_rowbatch_kernel(
   }
 }
 
+
+// ---------------------------------------------------------------- spread_rb2
+// Second-generation batch adjoint (same contract as spread_rowbatch_kernel:
+// owner-computes, lanes = batch vectors, every cell written once with a plain
+// coalesced store; no atomics, no zero pass).
+//
+// The CTA owns R consecutive output rows y0 .. y0 + R - 1, cells [c0, c0 + S),
+// for one 32-vector chunk. Its nodes are those of the 2m + R - 1 window rows
+// a = y0 - m + r, columns [c0 - m, c0 + S + m - 2]: per window row ONE
+// contiguous range of the cell-sorted order (two when the window wraps around
+// the torus). The window rows' ranges, concatenated, form one virtual node
+// sequence that the CTA's warps split EVENLY, so the dense centre of a radial
+// trajectory spreads over all warps of its CTA instead of serialising one warp
+// per window row. A warp walks its slice in chunks of CH nodes staged with
+// cp.async into a per-warp double buffer (values f^T[pos][b], taps
+// wt[pos][d][t], last-dimension cells cl[pos]): the next chunk is in flight
+// while the current one is accumulated. Window row r gives output row j the
+// dimension-0 tap 2m - 1 - r + j (zero outside [0, 2m)); the
+// node's window column u = cl + shift in [0, S + 2m - 1) selects, through a
+// warp-uniform switch, a compile-time body that adds v w0_j w1[t] to exactly the
+// cells the node reaches along the last dimension; fp32 multiply-adds are
+// packed FFMA2. The warps' partial rows are summed in shared memory (aliasing
+// the staging buffers), one output row at a time, and stored coalesced.
+#ifndef NFFTB_RB2_R
+#define NFFTB_RB2_R 2
+#endif
+#ifndef NFFTB_RB2_SF
+#define NFFTB_RB2_SF 16
+#endif
+#ifndef NFFTB_RB2_CHF
+#define NFFTB_RB2_CHF 16
+#endif
+#ifndef NFFTB_RB2_MINB
+#define NFFTB_RB2_MINB 2
+#endif
+constexpr int RB2_WARPS = 8;
+template <typename T> struct Rb2Cfg {
+  static constexpr int R = sizeof(T) == 4 ? NFFTB_RB2_R : 1;    // output rows per CTA
+  static constexpr int S = sizeof(T) == 4 ? NFFTB_RB2_SF : 16;  // output cells per CTA (last dimension)
+  static constexpr int CH = sizeof(T) == 4 ? NFFTB_RB2_CHF : 8;  // staged nodes per chunk
+};
+
+__host__ __device__ constexpr size_t rb2_al16(size_t b) { return (b + 15) & ~(size_t)15; }
+// one staging buffer of a warp: values, tap rows (both dimensions), cells
+__host__ __device__ constexpr size_t rb2_vbytes(int CH, size_t csize) { return (size_t)CH * 32 * csize; }
+// staged tap record of a node: 2m dimension-0 taps, 2m last-dimension taps, 16 zero bytes (the row tap of
+// a window row that does not reach an output row reads the zeros: no predicated loads)
+__host__ __device__ constexpr int rb2_rec(int M, size_t rsize) { return 4 * M + (int)(16 / rsize); }
+__host__ __device__ constexpr size_t rb2_wbytes(int CH, int M, size_t rsize) { return (size_t)CH * rb2_rec(M, rsize) * rsize; }
+__host__ __device__ constexpr size_t rb2_buf_bytes(int CH, int M, size_t csize, size_t rsize) {
+  return rb2_al16(rb2_vbytes(CH, csize)) + rb2_al16(rb2_wbytes(CH, M, rsize)) + rb2_al16((size_t)CH * 4);
+}
+__host__ __device__ inline size_t rb2_smem_bytes(int M, int rsize) {
+  const bool f32 = rsize == 4;
+  const int CH = f32 ? Rb2Cfg<float>::CH : Rb2Cfg<double>::CH, S = f32 ? Rb2Cfg<float>::S : Rb2Cfg<double>::S;
+  const size_t csize = 2 * (size_t)rsize;
+  const size_t stage = (size_t)RB2_WARPS * 2 * rb2_buf_bytes(CH, M, csize, rsize);
+  const size_t part = (size_t)RB2_WARPS * S * RB_PITCH * csize;  // one output row's partials
+  return stage > part ? stage : part;
+}
+
+// the cells k of the segment reached by a node in window column U (compile-time):
+// acc[j][k] += w1[k - U + 2m - 1] * vw[j]
+template <typename T, int M, int R, int S, int U>
+__device__ __forceinline__ void rb2_cells(typename cplx<T>::type (&acc)[R][S], const typename cplx<T>::type (&vw)[R],
+                                          const T (&w1)[2 * M]) {
+  constexpr int TAPS = 2 * M;
+  constexpr int KLO = U - TAPS + 1 > 0 ? U - TAPS + 1 : 0;
+  constexpr int KHI = U < S - 1 ? U : S - 1;
+#pragma unroll
+  for (int k = KLO; k <= KHI; ++k) {
+    const T w = w1[k - U + TAPS - 1];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if constexpr (sizeof(T) == 4) {
+        acc[j][k] = __ffma2_rn(make_float2(w, w), vw[j], acc[j][k]);
+      } else {
+        acc[j][k].x = fma(w, vw[j].x, acc[j][k].x);
+        acc[j][k].y = fma(w, vw[j].y, acc[j][k].y);
+      }
+    }
+  }
+}
+
+// one node (staged slot q) in window column U: value, row taps (zero where window row p does not
+// reach output row j), last-dimension taps, then the compile-time cell body
+template <typename T, int M, int R, int S, int U>
+__device__ __forceinline__ void rb2_visit(typename cplx<T>::type (&acc)[R][S], const typename cplx<T>::type* sv,
+                                          const T* sw, const int (&tj)[R]) {
+  using C = typename cplx<T>::type;
+  constexpr int TAPS = 2 * M;
+  T w1[TAPS];
+  if constexpr ((TAPS * sizeof(T)) % 16 == 0) {
+#pragma unroll
+    for (int t = 0; t < TAPS; t += 16 / (int)sizeof(T)) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 v4 = *reinterpret_cast<const float4*>(sw + TAPS + t);
+        w1[t] = v4.x; w1[t + 1] = v4.y; w1[t + 2] = v4.z; w1[t + 3] = v4.w;
+      } else {
+        const double2 v2 = *reinterpret_cast<const double2*>(sw + TAPS + t);
+        w1[t] = v2.x; w1[t + 1] = v2.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < TAPS; ++t) w1[t] = sw[TAPS + t];
+  }
+  const C v = *sv;
+  C vw[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const T w0 = sw[tj[j]];
+    if constexpr (sizeof(T) == 4) {
+      vw[j] = __fmul2_rn(make_float2(w0, w0), v);
+    } else {
+      vw[j].x = w0 * v.x;
+      vw[j].y = w0 * v.y;
+    }
+  }
+  rb2_cells<T, M, R, S, U>(acc, vw, w1);
+}
+
+// window column U of the fall-through walk: visit the chunk's nodes with u == U, then fall into U + 1
+#define NFFTB_RB2_STEP(U)                                                                       \
+  case U:                                                                                       \
+    if constexpr (U < S + 2 * M - 1) {                                                          \
+      while (uq == U) {                                                                         \
+        rb2_visit<T, M, R, S, U>(acc, sv + q * 32, sw + q * REC, tj);                           \
+        if (++q == cnt) goto chunk_done;                                                        \
+        uq = sc[q] + sh;                                                                        \
+      }                                                                                         \
+    }                                                                                           \
+    [[fallthrough]];
+
+template <typename T, int M>
+__global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_kernel(
+    Geom g, const typename cplx<T>::type* __restrict__ fTc, int BP, const T* __restrict__ wt,
+    const int* __restrict__ cl, const int* __restrict__ cstart, typename cplx<T>::type* __restrict__ grid) {
+  using C = typename cplx<T>::type;
+  constexpr int TAPS = 2 * M, R = Rb2Cfg<T>::R, S = Rb2Cfg<T>::S, CH = Rb2Cfg<T>::CH, NW = RB2_WARPS;
+  constexpr int WR = TAPS + R - 1;  // window rows (lane r describes window row r)
+  constexpr int REC = rb2_rec(M, sizeof(T));
+  static_assert(WR <= 32, "window rows per warp");
+  static_assert(S + 2 * M - 1 <= 48, "switch cases");
+  constexpr size_t VB = rb2_al16(rb2_vbytes(CH, sizeof(C))), WB = rb2_al16(rb2_wbytes(CH, M, sizeof(T)));
+  constexpr size_t BUF = rb2_buf_bytes(CH, M, sizeof(C), sizeof(T));
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b0 = blockIdx.y * RB_LANES;
+  const int Nt0 = g.Nt[0], NtL = g.Nt[1];
+  const int nseg = (NtL + S - 1) / S;
+  const int yb = blockIdx.x / nseg;
+  const int y0 = yb * R, c0 = (blockIdx.x - yb * nseg) * S;
+  const int qs = min(S, NtL - c0);
+  // 1. window row r = lane: part 0 (unwrapped columns) [lo0, lo0 + len0) with column shift sh0, part 1
+  //    (the columns wrapped around the torus) [lo1, lo1 + len1) with shift sh1
+  int lo0 = 0, len0 = 0, sh0 = 0, lo1 = 0, len1 = 0, sh1 = 0;
+  if (lane < WR) {
+    int a = y0 - M + lane;
+    if (a < 0) a += Nt0;
+    else if (a >= Nt0) a -= Nt0;
+    const long long rowkey = (long long)a * NtL;
+    const int lo_c = c0 - M, hi_c = c0 + qs + M - 1;  // unwrapped window columns [lo_c, hi_c)
+    {
+      const int ca = max(lo_c, 0), cb = min(hi_c, NtL);
+      lo0 = __ldg(cstart + rowkey + ca);
+      len0 = __ldg(cstart + rowkey + cb) - lo0;
+      sh0 = -lo_c;
+    }
+    int ca = 0, cb = 0;
+    if (lo_c < 0) {
+      ca = lo_c + NtL;
+      cb = NtL;
+      sh1 = -lo_c - NtL;
+    } else if (hi_c > NtL) {
+      ca = 0;
+      cb = hi_c - NtL;
+      sh1 = NtL - lo_c;
+    }
+    if (ca < cb) {
+      lo1 = __ldg(cstart + rowkey + ca);
+      len1 = __ldg(cstart + rowkey + cb) - lo1;
+    }
+  }
+  int total;
+  const int roff = warp_exclusive_scan(len0 + len1, total);
+  // this warp's slice [vs, ve) of the virtual sequence
+  const int vs = (int)(((long long)total * warp) / NW), ve = (int)(((long long)total * (warp + 1)) / NW);
+  C acc[R][S];
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      acc[j][k].x = (T)0;
+      acc[j][k].y = (T)0;
+    }
+  unsigned char* wbase = smem_raw + (size_t)warp * 2 * BUF;
+  fTc += b0;
+  // a chunk: window row p, virtual start x (roff_p <= x), cnt nodes, never straddling a part
+  struct Chunk {
+    int p, x, cnt, pos0, sh;
+  };
+  auto make_chunk = [&](int x, int p) {  // the chunk starting at x (< ve), searching rows from p
+    Chunk c;
+    int o, l0, l1;
+    while (true) {
+      o = __shfl_sync(0xffffffffu, roff, p);
+      l0 = __shfl_sync(0xffffffffu, len0, p);
+      l1 = __shfl_sync(0xffffffffu, len1, p);
+      if (x < o + l0 + l1) break;
+      ++p;
+    }
+    const int lo_0 = __shfl_sync(0xffffffffu, lo0, p), lo_1 = __shfl_sync(0xffffffffu, lo1, p);
+    const int s_0 = __shfl_sync(0xffffffffu, sh0, p), s_1 = __shfl_sync(0xffffffffu, sh1, p);
+    const int off = x - o;
+    c.p = p;
+    c.x = x;
+    if (off < l0) {
+      c.pos0 = lo_0 + off;
+      c.sh = s_0;
+      c.cnt = min(min(CH, l0 - off), ve - x);
+    } else {
+      c.pos0 = lo_1 + (off - l0);
+      c.sh = s_1;
+      c.cnt = min(min(CH, l0 + l1 - off), ve - x);
+    }
+    return c;
+  };
+  auto stage = [&](const Chunk& c, int buf) {
+    unsigned char* sb = wbase + (size_t)buf * BUF;
+    constexpr int VP = 32 * (int)sizeof(C) / 16;  // 16-byte pieces per value row
+    for (int e = lane; e < c.cnt * VP; e += 32) {
+      const int q = e / VP, pc = e - q * VP;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(sb + (size_t)q * 32 * sizeof(C) + pc * 16);
+      const void* src = reinterpret_cast<const unsigned char*>(fTc + (long long)(c.pos0 + q) * BP) + pc * 16;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src) : "memory");
+    }
+    // tap records: the node's 2 * TAPS reals (a 16-byte multiple, contiguous for consecutive positions)
+    // and one zero-filled piece (source size 0)
+    constexpr int WP = 2 * TAPS * (int)sizeof(T) / 16 + 1;  // pieces per record
+    const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(wt + (long long)c.pos0 * 2 * TAPS);
+    for (int e = lane; e < c.cnt * WP; e += 32) {
+      const int q = e / WP, pc = e - q * WP;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(sb + VB + (size_t)e * 16);
+      const unsigned char* src = wsrc + (size_t)q * 2 * TAPS * sizeof(T) + pc * 16;
+      const int nbytes = pc < WP - 1 ? 16 : 0;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
+    }
+    if (lane < c.cnt) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(sb + VB + WB + (size_t)lane * 4);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(cl + c.pos0 + lane) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // f^T comes from transpose_bm
+  if (vs < ve) {
+    Chunk cur = make_chunk(vs, 0);
+    int buf = 0;
+    stage(cur, 0);
+    while (true) {
+      Chunk nxt;
+      nxt.cnt = 0;
+      const int xn = cur.x + cur.cnt;
+      if (xn < ve) {
+        nxt = make_chunk(xn, cur.p);
+        stage(nxt, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncwarp();
+      {  // accumulate the current chunk
+        const unsigned char* sb = wbase + (size_t)buf * BUF;
+        const C* sv = reinterpret_cast<const C*>(sb) + lane;
+        const T* sw = reinterpret_cast<const T*>(sb + VB);
+        const int* sc = reinterpret_cast<const int*>(sb + VB + WB);
+        int tj[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int t = TAPS - 1 - cur.p + j;
+          tj[j] = (unsigned)t < (unsigned)TAPS ? t : 2 * TAPS;  // out of reach: the record's zeros
+        }
+        // the chunk's nodes lie in one window row part, in column order: u is non-decreasing, so the
+        // walk enters the unrolled sequence of window columns once (switch on the first node's u) and
+        // falls through it, each column U visiting its nodes with a compile-time body
+        const int sh = cur.sh, cnt = cur.cnt;
+        int q = 0, uq = sc[0] + sh;
+        switch (uq) {
+          NFFTB_RB2_STEP(0) NFFTB_RB2_STEP(1) NFFTB_RB2_STEP(2) NFFTB_RB2_STEP(3) NFFTB_RB2_STEP(4)
+          NFFTB_RB2_STEP(5) NFFTB_RB2_STEP(6) NFFTB_RB2_STEP(7) NFFTB_RB2_STEP(8) NFFTB_RB2_STEP(9)
+          NFFTB_RB2_STEP(10) NFFTB_RB2_STEP(11) NFFTB_RB2_STEP(12) NFFTB_RB2_STEP(13) NFFTB_RB2_STEP(14)
+          NFFTB_RB2_STEP(15) NFFTB_RB2_STEP(16) NFFTB_RB2_STEP(17) NFFTB_RB2_STEP(18) NFFTB_RB2_STEP(19)
+          NFFTB_RB2_STEP(20) NFFTB_RB2_STEP(21) NFFTB_RB2_STEP(22) NFFTB_RB2_STEP(23) NFFTB_RB2_STEP(24)
+          NFFTB_RB2_STEP(25) NFFTB_RB2_STEP(26) NFFTB_RB2_STEP(27) NFFTB_RB2_STEP(28) NFFTB_RB2_STEP(29)
+          NFFTB_RB2_STEP(30) NFFTB_RB2_STEP(31) NFFTB_RB2_STEP(32) NFFTB_RB2_STEP(33) NFFTB_RB2_STEP(34)
+          NFFTB_RB2_STEP(35) NFFTB_RB2_STEP(36) NFFTB_RB2_STEP(37) NFFTB_RB2_STEP(38) NFFTB_RB2_STEP(39)
+          NFFTB_RB2_STEP(40) NFFTB_RB2_STEP(41) NFFTB_RB2_STEP(42) NFFTB_RB2_STEP(43) NFFTB_RB2_STEP(44)
+          NFFTB_RB2_STEP(45) NFFTB_RB2_STEP(46) NFFTB_RB2_STEP(47)
+          default: break;
+        }
+      chunk_done:;
+      }
+      __syncwarp();  // the buffer is consumed before it is restaged
+      if (nxt.cnt == 0) break;
+      cur = nxt;
+      buf ^= 1;
+    }
+  }
+  // 2. sum the warps' partial rows in shared memory (aliasing the staging buffers), one output row at a
+  //    time; one coalesced store per output cell and vector
+  const int nbc = min(RB_LANES, g.B - b0);
+  int cs0 = c0 - (NtL >> 1);
+  if (cs0 < 0) cs0 += NtL;
+  C* part = reinterpret_cast<C*>(smem_raw);  // [NW][S][RB_PITCH]
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    __syncthreads();  // staging buffers / the previous row's partials are consumed
+#pragma unroll
+    for (int k = 0; k < S; ++k) part[((size_t)warp * S + k) * RB_PITCH + lane] = acc[j][k];
+    __syncthreads();
+    const int y = y0 + j;
+    if (y >= Nt0) break;
+    int ys = y - (Nt0 >> 1);
+    if (ys < 0) ys += Nt0;
+    const long long rowoff = (long long)ys * NtL;
+    for (int idx = tid; idx < nbc * S; idx += NW * 32) {
+      const int bb = idx / S, k = idx - bb * S;
+      if (k >= qs) continue;
+      C a;
+      a.x = (T)0;
+      a.y = (T)0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const C c = part[((size_t)w * S + k) * RB_PITCH + bb];
+        a.x += c.x;
+        a.y += c.y;
+      }
+      int cs = cs0 + k;
+      if (cs >= NtL) cs -= NtL;
+      grid[(long long)(b0 + bb) * g.grid_cells + rowoff + cs] = a;
+    }
+  }
+}
+#undef NFFTB_RB2_STEP
+
 }  // namespace nfftb
