@@ -434,41 +434,75 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
   const int b0 = blockIdx.y * RB_LANES;
   const int Nt0 = g.Nt[0], NtL = g.Nt[1];
   const int nseg = (NtL + S - 1) / S;
-  const int yb = blockIdx.x / nseg;
-  const int y0 = yb * R, c0 = (blockIdx.x - yb * nseg) * S;
-  const int qs = min(S, NtL - c0);
-  // 1. window row r = lane: part 0 (unwrapped columns) [lo0, lo0 + len0) with column shift sh0, part 1
-  //    (the columns wrapped around the torus) [lo1, lo1 + len1) with shift sh1
-  int lo0 = 0, len0 = 0, sh0 = 0, lo1 = 0, len1 = 0, sh1 = 0;
-  if (lane < WR) {
-    int a = y0 - M + lane;
-    if (a < 0) a += Nt0;
-    else if (a >= Nt0) a -= Nt0;
-    const long long rowkey = (long long)a * NtL;
-    const int lo_c = c0 - M, hi_c = c0 + qs + M - 1;  // unwrapped window columns [lo_c, hi_c)
-    {
-      const int ca = max(lo_c, 0), cb = min(hi_c, NtL);
-      lo0 = __ldg(cstart + rowkey + ca);
-      len0 = __ldg(cstart + rowkey + cb) - lo0;
-      sh0 = -lo_c;
+  const int nunits = (Nt0 + R - 1) / R * nseg;
+  const int nbc = min(RB_LANES, g.B - b0);
+  unsigned char* wbase = smem_raw + (size_t)warp * 2 * BUF;
+  fTc += b0;
+  // 1. window row r = lane of unit (y0, c0): part 0 (unwrapped columns) [lo0, lo0 + len0) with column
+  //    shift sh0, part 1 (the columns wrapped around the torus) [lo1, lo1 + len1) with shift sh1. The
+  //    four cstart values of the NEXT unit are loaded while the current unit is processed.
+  struct Raw {
+    int c[4];
+  };
+  auto unit_geom = [&](int unit, int& y0, int& c0, int& qs) {
+    const int yb = unit / nseg;
+    y0 = yb * R;
+    c0 = (unit - yb * nseg) * S;
+    qs = min(S, NtL - c0);
+  };
+  auto load_raw = [&](int unit) {
+    Raw rw;
+    rw.c[0] = rw.c[1] = rw.c[2] = rw.c[3] = 0;
+    if (unit < nunits && lane < WR) {
+      int y0, c0, qs;
+      unit_geom(unit, y0, c0, qs);
+      int a = y0 - M + lane;
+      if (a < 0) a += Nt0;
+      else if (a >= Nt0) a -= Nt0;
+      const long long rowkey = (long long)a * NtL;
+      const int lo_c = c0 - M, hi_c = c0 + qs + M - 1;
+      rw.c[0] = __ldg(cstart + rowkey + max(lo_c, 0));
+      rw.c[1] = __ldg(cstart + rowkey + min(hi_c, NtL));
+      if (lo_c < 0) {
+        rw.c[2] = __ldg(cstart + rowkey + lo_c + NtL);
+        rw.c[3] = __ldg(cstart + rowkey + NtL);
+      } else if (hi_c > NtL) {
+        rw.c[2] = __ldg(cstart + rowkey);
+        rw.c[3] = __ldg(cstart + rowkey + hi_c - NtL);
+      }
     }
-    int ca = 0, cb = 0;
-    if (lo_c < 0) {
-      ca = lo_c + NtL;
-      cb = NtL;
-      sh1 = -lo_c - NtL;
-    } else if (hi_c > NtL) {
-      ca = 0;
-      cb = hi_c - NtL;
-      sh1 = NtL - lo_c;
-    }
-    if (ca < cb) {
-      lo1 = __ldg(cstart + rowkey + ca);
-      len1 = __ldg(cstart + rowkey + cb) - lo1;
-    }
-  }
+    return rw;
+  };
+  int unit = blockIdx.x;
+  Raw raw = load_raw(unit);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // f^T comes from transpose_bm
+  for (; unit < nunits; unit += gridDim.x) {
+  int y0, c0, qs;
+  unit_geom(unit, y0, c0, qs);
+  const int lo_c = c0 - M;
+  const int lo0 = raw.c[0], len0 = raw.c[1] - raw.c[0], sh0 = -lo_c;
+  const int lo1 = raw.c[2], len1 = raw.c[3] - raw.c[2], sh1 = lo_c < 0 ? -lo_c - NtL : NtL - lo_c;
+  raw = load_raw(unit + gridDim.x);
   int total;
   const int roff = warp_exclusive_scan(len0 + len1, total);
+  int cs0 = c0 - (NtL >> 1);
+  if (cs0 < 0) cs0 += NtL;
+  if (total == 0) {  // no node reaches the unit (outside a radial trajectory's disk): zeros
+    for (int idx = tid; idx < R * nbc * S; idx += NW * 32) {
+      const int j = idx / (nbc * S), r2 = idx - j * (nbc * S), bb = r2 / S, k = r2 - bb * S;
+      const int y = y0 + j;
+      if (k >= qs || y >= Nt0) continue;
+      int ys = y - (Nt0 >> 1);
+      if (ys < 0) ys += Nt0;
+      int cs = cs0 + k;
+      if (cs >= NtL) cs -= NtL;
+      C z;
+      z.x = (T)0;
+      z.y = (T)0;
+      grid[(long long)(b0 + bb) * g.grid_cells + (long long)ys * NtL + cs] = z;
+    }
+    continue;
+  }
   // this warp's slice [vs, ve) of the virtual sequence
   const int vs = (int)(((long long)total * warp) / NW), ve = (int)(((long long)total * (warp + 1)) / NW);
   C acc[R][S];
@@ -479,8 +513,6 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
       acc[j][k].x = (T)0;
       acc[j][k].y = (T)0;
     }
-  unsigned char* wbase = smem_raw + (size_t)warp * 2 * BUF;
-  fTc += b0;
   // a chunk: window row p, virtual start x (roff_p <= x), cnt nodes, never straddling a part
   struct Chunk {
     int p, x, cnt, pos0, sh;
@@ -537,7 +569,6 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // f^T comes from transpose_bm
   if (vs < ve) {
     Chunk cur = make_chunk(vs, 0);
     int buf = 0;
@@ -593,9 +624,6 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
   }
   // 2. sum the warps' partial rows in shared memory (aliasing the staging buffers), one output row at a
   //    time; one coalesced store per output cell and vector
-  const int nbc = min(RB_LANES, g.B - b0);
-  int cs0 = c0 - (NtL >> 1);
-  if (cs0 < 0) cs0 += NtL;
   C* part = reinterpret_cast<C*>(smem_raw);  // [NW][S][RB_PITCH]
 #pragma unroll
   for (int j = 0; j < R; ++j) {
@@ -625,6 +653,8 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
       grid[(long long)(b0 + bb) * g.grid_cells + rowoff + cs] = a;
     }
   }
+  __syncthreads();  // the partials are consumed before the next unit stages into the same memory
+  }  // units
 }
 #undef NFFTB_RB2_STEP
 
