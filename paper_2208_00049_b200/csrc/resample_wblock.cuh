@@ -33,9 +33,18 @@
 
 namespace nfftb {
 
-constexpr int WB_K0 = 16;    // cells along dimension 0 per warp (registers)
-constexpr int WB_WARPS = 4;  // independent warps per CTA
-constexpr int WB_NB = 16;    // nodes per staged batch (two batches in flight per warp)
+#ifndef NFFTB_WB_K0
+#define NFFTB_WB_K0 16
+#endif
+#ifndef NFFTB_WB_WARPS
+#define NFFTB_WB_WARPS 4
+#endif
+#ifndef NFFTB_WB_NB
+#define NFFTB_WB_NB 16
+#endif
+constexpr int WB_K0 = NFFTB_WB_K0;        // cells along dimension 0 per warp (registers)
+constexpr int WB_WARPS = NFFTB_WB_WARPS;  // independent warps per CTA
+constexpr int WB_NB = NFFTB_WB_NB;        // nodes per staged batch (two batches in flight per warp)
 
 template <typename T, int D, int M>
 struct WbCfg {

@@ -7,7 +7,7 @@ cp paper_2208_00049_b200/libnfft_b200.so /tmp/product.so
 for v in product "$@"; do
   tag=$(basename $v .so)
   [ "$v" != product ] && cp $v paper_2208_00049_b200/libnfft_b200.so
-  timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "batch_adjoint or radial_batch" > $out/t_$tag.log 2>&1
+  timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "${TESTK:-batch_adjoint or radial_batch}" > $out/t_$tag.log 2>&1
   echo "$tag pytest $?" >> $out/summary.txt
   bash tools/quick_bench.sh $out/qb_$tag $cfgs | sed "s/^/$tag /" >> $out/summary.txt
   cp /tmp/product.so paper_2208_00049_b200/libnfft_b200.so
