@@ -36,9 +36,8 @@ struct KernelSet {
   const void* full_interp;
   const void* full_spread;  // D >= 2
   const void* spread_cell;  // takes WinPolyN<T, D, m> (launched with launch_k)
-  // D = 2 batches: row-segment spread, lanes = batch vectors (resample_rowbatch.cuh)
-  void (*spread_rowbatch)(Geom, const C*, int, const T*, const int*, C*);
-  // second generation: parts split evenly over the warps, cp.async-staged chunks, FFMA2
+  // D = 2 batches: lanes = batch vectors, window-row parts split evenly over the warps, cp.async-staged
+  // chunks, FFMA2 (resample_rowbatch.cuh)
   void (*spread_rb2)(Geom, const C*, int, const T*, const int*, const int*, C*);
   const void* taps_nd;  // takes WinPolyN<T, D, m> (launched with launch_k)
   // D = 2, 3: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
@@ -102,7 +101,6 @@ KernelSet<T> make_set() {
     k.full_spread = (const void*)full_spread_kernel<T, D, M>;
     k.spread_cell = (const void*)spread_cell_kernel<T, D, M, DEG>;
     if constexpr (D == 2) {
-      k.spread_rowbatch = spread_rowbatch_kernel<T, M>;
       k.spread_rb2 = spread_rb2_kernel<T, M>;
     }
     k.taps_nd = (const void*)taps_nd_kernel<T, D, M, DEG>;
