@@ -31,6 +31,7 @@ struct KernelSet {
   // D = 2, 3 over cell-sorted nodes (resample_cell.cuh)
   const void* interp_cell;  // takes WinPolyN<T, D, m> (launched with launch_k)
   const void* interp_cellt;  // TENSOR: taps from the stored table
+  const void* interp_cell2;  // fp32 2D batches: two vectors per CTA
   // FULL precompute strategy (resample_full.cuh): the sparse matrix B
   const void* full_build;
   const void* full_interp;
@@ -98,6 +99,7 @@ KernelSet<T> make_set() {
   } else {
     k.interp_cell = (const void*)interp_cell_kernel<T, D, M, DEG, false>;
     k.interp_cellt = (const void*)interp_cell_kernel<T, D, M, DEG, true>;
+    if constexpr (D == 2 && sizeof(T) == 4) k.interp_cell2 = (const void*)interp_cell2_kernel<M, DEG>;
     k.full_spread = (const void*)full_spread_kernel<T, D, M>;
     k.spread_cell = (const void*)spread_cell_kernel<T, D, M, DEG>;
     if constexpr (D == 2) {

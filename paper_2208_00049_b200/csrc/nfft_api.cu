@@ -107,6 +107,7 @@ struct nfft_plan_s {
   void* d_fT = nullptr;      // M * bp complex: node values, transposed (node-major)
   size_t rb_bytes = 0;
   int rb_occ = 1;            // resident spread_rb2 CTAs per SM (persistent launch width)
+  bool cell2 = false;        // fp32 2D batches: interp_cell2 (two vectors per CTA)
   bool wbmode = false;       // D = 2, 3 cell mode: warp-owned cell blocks over the TENSOR taps (resample_wblock.cuh)
   size_t wb_bytes = 0;
   void* d_fc = nullptr;      // B * M complex: node values in cell order (warp-block adjoint)
@@ -462,6 +463,20 @@ nfft_status configure_kernels(nfft_plan p, const KernelSet<T>& ks) {
     }
     p->batchmode = ok;
   }
+  // fp32 batches: two vectors per interpolation CTA, on grids with at most one node per cell (radial
+  // sigma = 2: 195 -> 170 us). Denser grids keep one vector per CTA: there the dense centre's tiles set
+  // the tail and twice the work per CTA costs more than the shared taps save (sigma = 1.25, 2 nodes per
+  // cell: 162 vs 173 us)
+  if (p->batchmode && !p->tensor && ks.interp_cell2 && p->M <= p->ncells) {
+    int o = 0;
+    p->cell2 = p->cellmode && 2 * p->region_bytes <= 200 * 1024 &&
+               cudaFuncSetAttribute(ks.interp_cell2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(2 * p->region_bytes)) == cudaSuccess &&
+               cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ks.interp_cell2, RC_THREADS, 2 * p->region_bytes) ==
+                   cudaSuccess &&
+               o >= 1;
+    cudaGetLastError();
+  }
   if (p->wbmode) {
     bool ok = p->cellmode && !p->batchmode && ks.spread_wb;
     if (ok) {
@@ -723,6 +738,12 @@ nfft_status stage_interp(nfft_plan p, typename cplx<T>::type* f, cudaStream_t st
                                                                            (int64_t)p->sm_count * 16));
     CK(launch_k(ks.full_interp, dim3(ctas, (unsigned)p->B), FI_THREADS, 0, st, p->geom, grid, (const T*)p->d_bw,
                 (const int*)p->d_bi, (const int*)p->d_jc, p->node_begin, p->node_end, f));
+  } else if (p->cell2) {
+    using C = typename cplx<T>::type;
+    CK((pdl ? launch_k_pdl<Geom, WpnArg, const C*, const T*, const int*, const int*, C*>
+            : launch_k<Geom, WpnArg, const C*, const T*, const int*, const int*, C*>)(
+        ks.interp_cell2, dim3((unsigned)p->n_tiles, (unsigned)((p->B + 1) / 2)), RC_THREADS, 2 * p->region_bytes, st,
+        p->geom, wpn, grid, (const T*)p->d_kc, (const int*)p->d_jc, (const int*)p->d_cstart, f));
   } else if (p->cellmode && p->D >= 2) {
     CK((pdl ? launch_k_pdl<Geom, WpnArg, const typename cplx<T>::type*, const T*, const T*, const int*, const int*, int,
                            int, typename cplx<T>::type*>
@@ -1131,7 +1152,8 @@ nfft_status create_impl(nfft_plan* out, int D, const int64_t* N, int64_t M, cons
     region_cells = 1;
     for (int d = 0; d < D; ++d) {
       Lreg[d] = Q[d] + 2 * m - 1;
-      if (d == D - 1 && precision == NFFT_COMPLEX128) {
+      // (also fp32 2D batches: interp_cell2's 16-byte elements rotate the same way)
+      if (d == D - 1 && (precision == NFFT_COMPLEX128 || (D == 2 && opt.batch >= 8))) {
         const int64_t tp = 2 * m <= 8 ? 8 : 16;
         Lreg[d] = ((Q[d] + tp - 1) + 7) / 8 * 8;
       }

@@ -217,6 +217,155 @@ __global__ void __launch_bounds__(RC_THREADS, D == 2 ? 4 : 2) interp_cell_kernel
   }
 }
 
+// interp_cell2: the same forward interpolation for fp32 2D BATCHES with TWO
+// vectors per CTA (config 5). The region is staged interleaved, one 16-byte
+// element (vector b, vector b + 1) per cell, so the node's position, taps
+// (evaluated once for both vectors) and the (2m)^2 region reads (LDS.128: 8
+// lanes per shared-memory phase, half the conflict exposure of 16 lanes of
+// 8-byte reads) serve two outputs; the multiply-adds are packed FFMA2.
+#ifndef NFFTB_IC2_MINB
+#define NFFTB_IC2_MINB 3
+#endif
+template <int M, int DEG>
+__global__ void __launch_bounds__(RC_THREADS, NFFTB_IC2_MINB) interp_cell2_kernel(Geom g, WinPolyN<float, 2, M> wp,
+                                                                     const float2* __restrict__ grid,
+                                                                     const float* __restrict__ kc,
+                                                                     const int* __restrict__ jc,
+                                                                     const int* __restrict__ cstart,
+                                                                     float2* __restrict__ f) {
+  constexpr int EXT = 2 * M - 1;
+  constexpr int MAXROWS = 1024;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int rpre[MAXROWS + 1];
+  __shared__ int rbeg[MAXROWS];
+  __shared__ int ws[32];
+  float4* tile = reinterpret_cast<float4*>(smem_raw);  // [region cell] = (vector b0, vector b0 + 1)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int c0[2], s0[2], Rr[2], Qt[2];
+  {
+    int rem = blockIdx.x;
+#pragma unroll
+    for (int d = 1; d >= 0; --d) {
+      const int p = rem % g.P[d];
+      rem /= g.P[d];
+      c0[d] = p * g.Q[d];
+      Qt[d] = min(g.Q[d], g.Nt[d] - c0[d]);
+      Rr[d] = Qt[d] + EXT;
+      s0[d] = pos_mod(c0[d] - M + 1 - (g.Nt[d] >> 1), g.Nt[d]);
+    }
+  }
+  const int Lp = g.L[1];
+  const int b0 = blockIdx.y * 2;
+  const bool two = b0 + 1 < g.B;
+  // the tile's nodes: one cell-sorted range per tile row (overlaps the FFT's tail under PDL)
+  const int nrows = Qt[0];
+  {
+    const int per = (nrows + RC_THREADS - 1) / RC_THREADS;
+    const int lo = threadIdx.x * per, hi = min(nrows, lo + per);
+    int cnt = 0;
+    for (int r = lo; r < hi; ++r) {
+      const long long key = (long long)(c0[0] + r) * g.Nt[1] + c0[1];
+      const int a = cstart[key], b = cstart[key + Qt[1]];
+      rbeg[r] = a;
+      rpre[r] = b - a;
+      cnt += b - a;
+    }
+    int tot;
+    int run = block_exclusive_scan(cnt, ws, tot);
+    for (int r = lo; r < hi; ++r) {
+      const int c = rpre[r];
+      rpre[r] = run;
+      run += c;
+    }
+    if (threadIdx.x == 0) rpre[nrows] = tot;
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the grid (previous kernel's output) is complete
+  {  // stage both vectors' regions, interleaved (8-byte cp.async per cell and vector; zero fill past B)
+    const float2* g0 = grid + (long long)b0 * g.grid_cells;
+    const float2* g1 = two ? g0 + g.grid_cells : g0;
+    const int NtL = g.Nt[1];
+    int sa = s0[0] + warp;
+    while (sa >= g.Nt[0]) sa -= g.Nt[0];
+    for (int r = warp; r < Rr[0]; r += RC_THREADS / 32) {
+      const long long off = (long long)sa * NtL;
+      for (int col = lane; col < Rr[1]; col += 32) {
+        int sc = s0[1] + col;
+        while (sc >= NtL) sc -= NtL;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(tile + (size_t)r * Lp + col);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(g0 + off + sc) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d + 8), "l"(g1 + off + sc),
+                     "r"(two ? 8 : 0)
+                     : "memory");
+      }
+      sa += RC_THREADS / 32;
+      while (sa >= g.Nt[0]) sa -= g.Nt[0];
+    }
+  }
+  const int total = rpre[nrows];
+  auto position = [&](int q) {
+    int lo = 0, hi = nrows;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (rpre[mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    return rbeg[lo] + (q - rpre[lo]);
+  };
+  const int q0 = threadIdx.x;
+  const int pos0 = q0 < total ? position(q0) : 0;
+  const int j0 = q0 < total ? jc[pos0] : -1;
+  cp_async_wait_all();
+  __syncthreads();
+  float2* f0 = f + (long long)b0 * g.M;
+  for (int q = q0; q < total; q += RC_THREADS) {
+    const int pos = q == q0 ? pos0 : position(q);
+    const int j = q == q0 ? j0 : jc[pos];
+    int loc[2];
+    float w[2][2 * M];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      double frac;
+      loc[d] = node_cell((double)kc[(long long)d * g.M + pos], g.Ntd[d], g.Nt[d], frac) - c0[d];
+      window_taps<float, M, DEG>((float)(frac - 0.5), wp.mu[d], w[d]);
+    }
+    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+    // 2m = 8 or 16: bank rotation. Lane L reads element (k + rot) mod 2m at step k, rot = (L - loc) mod 2m,
+    // so with a pitch that is a multiple of 8 elements the 8 lanes of each 16-byte shared-memory phase
+    // touch 8 distinct bank quads whatever the node positions (the taps rotate with them)
+    constexpr bool ROT = 2 * M == 8 || 2 * M == 16;
+    float wl[2 * M];
+    int off[2 * M];
+    if constexpr (ROT) {
+      const int rot = (lane - loc[1]) & (2 * M - 1);
+      rotate_taps<float, M, 2 * M>(w[1], rot, wl);
+#pragma unroll
+      for (int k = 0; k < 2 * M; ++k) off[k] = (k + rot) & (2 * M - 1);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2 * M; ++k) {
+        wl[k] = w[1][k];
+        off[k] = k;
+      }
+    }
+#pragma unroll
+    for (int l0 = 0; l0 < 2 * M; ++l0) {
+      const float4* row = tile + (loc[0] + l0) * Lp + loc[1];
+      float2 s0v = make_float2(0.f, 0.f), s1v = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 2 * M; ++k) {
+        const float4 v = row[off[k]];
+        s0v = __ffma2_rn(make_float2(wl[k], wl[k]), make_float2(v.x, v.y), s0v);
+        s1v = __ffma2_rn(make_float2(wl[k], wl[k]), make_float2(v.z, v.w), s1v);
+      }
+      a0 = __ffma2_rn(make_float2(w[0][l0], w[0][l0]), s0v, a0);
+      a1 = __ffma2_rn(make_float2(w[0][l0], w[0][l0]), s1v, a1);
+    }
+    f0[j] = a0;
+    if (two) f0[g.M + j] = a1;
+  }
+}
+
 // ---------------------------------------------------------------- adjoint
 // shared memory per staged node slot (host and device agree)
 template <typename T, int D, int M>
