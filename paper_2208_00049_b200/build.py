@@ -53,7 +53,8 @@ def build(force=False, jobs=None, verbose=True, defines=(), out=None):
     global OBJ, LIB
     if defines or out:
         tag = "_".join(d.replace("=", "") for d in defines) or "x"
-        OBJ, LIB = os.path.join(ROOT, "build", "obj_" + tag), out or os.path.join(HERE, f"libnfft_b200_{tag}.so")
+        # experiment objects outside the repo (the repo snapshot travels to the GPU box)
+        OBJ, LIB = os.path.join("/tmp", "nfftb_obj_" + tag), out or os.path.join(HERE, f"libnfft_b200_{tag}.so")
     if not force and up_to_date():
         if verbose:
             print(f"[build] {LIB} up to date")
