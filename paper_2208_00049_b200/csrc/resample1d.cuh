@@ -163,8 +163,17 @@ constexpr int S1_CAP = 320;               // staged nodes per chunk (mean ~0.5 (
 // 4 per SM 10.5 us (3: 12.7, 2: 14.1); in the bench step with the direct NFFT running concurrently
 // (nfft_execute) the 121-register kernel at 4 per SM fills the register file and keeps the forward
 // FFT off the SMs (step 53.1 us), 3 per SM leaves it room (45.0 us). Hence two launch widths.
-constexpr int S1_CTAS_ALONE = 4;
-constexpr int S1_CTAS_OVERLAP = 3;
+#ifndef NFFTB_S1_ALONE
+#define NFFTB_S1_ALONE 4
+#endif
+#ifndef NFFTB_S1_OVERLAP
+#define NFFTB_S1_OVERLAP 3
+#endif
+#ifndef NFFTB_S1_MINB
+#define NFFTB_S1_MINB 1
+#endif
+constexpr int S1_CTAS_ALONE = NFFTB_S1_ALONE;
+constexpr int S1_CTAS_OVERLAP = NFFTB_S1_OVERLAP;
 
 // tap row pitch: 2m taps, odd pitch (neighbouring rows in distinct banks)
 __host__ __device__ constexpr int s1_pitch(int M) { return 2 * M + 1; }
@@ -179,7 +188,7 @@ __host__ __device__ inline size_t s1_smem_bytes(int M, size_t csize, size_t rsiz
 }
 
 template <typename T, int M, int DEG, bool TENSOR>
-__global__ void __launch_bounds__(S1_THREADS) spread1s_kernel(Geom g, WinPolyN<T, 1, M> wp,
+__global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geom g, WinPolyN<T, 1, M> wp,
                                                               const typename cplx<T>::type* __restrict__ f,
                                                               const T* __restrict__ kc, const T* __restrict__ wt,
                                                               const int* __restrict__ jc,
