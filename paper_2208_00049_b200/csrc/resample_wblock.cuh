@@ -42,6 +42,10 @@ namespace nfftb {
 #ifndef NFFTB_WB_NB
 #define NFFTB_WB_NB 16
 #endif
+#ifndef NFFTB_WB_UNROLL
+#define NFFTB_WB_UNROLL 2
+#endif
+constexpr int WB_UNROLL = NFFTB_WB_UNROLL;  // node visits unrolled per loop iteration
 constexpr int WB_K0 = NFFTB_WB_K0;        // cells along dimension 0 per warp (registers)
 constexpr int WB_WARPS = NFFTB_WB_WARPS;  // independent warps per CTA
 constexpr int WB_NB = NFFTB_WB_NB;        // nodes per staged batch (two batches in flight per warp)
@@ -115,7 +119,7 @@ __device__ __forceinline__ void wb_visit(int nn, const unsigned char* __restrict
   constexpr int TAPS = 2 * M;
   constexpr int KLO = U0 - TAPS + 1 > 0 ? U0 - TAPS + 1 : 0;
   constexpr int KHI = U0 < WB_K0 - 1 ? U0 : WB_K0 - 1;
-#pragma unroll 2
+#pragma unroll(WB_UNROLL)
   for (int n = 0; n < nn; ++n) {
     const unsigned char* sl = buf + n * Cfg::SLOT;
     const T* w = reinterpret_cast<const T*>(sl);
