@@ -269,9 +269,10 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
   const int nbc = min(RB_LANES, g.B - b0);
   unsigned char* wbase = smem_raw + (size_t)warp * 2 * BUF;
   fTc += b0;
-  // 1. window row r = lane of unit (y0, c0): part 0 (unwrapped columns) [lo0, lo0 + len0) with column
-  //    shift sh0, part 1 (the columns wrapped around the torus) [lo1, lo1 + len1) with shift sh1. The
-  //    four cstart values of the NEXT unit are loaded while the current unit is processed.
+  // 1. window row r = lane of this CTA's unit (y0, c0): part 0 (unwrapped columns) [lo0, lo0 + len0)
+  //    with column shift sh0, part 1 (the columns wrapped around the torus) [lo1, lo1 + len1) with shift
+  //    sh1. One CTA per unit (a persistent launch with the next unit prefetched measured slower, both
+  //    with a static and with a dynamic unit order: DESIGN.md §6).
   struct Raw {
     int c[4];
   };
@@ -304,16 +305,15 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
     }
     return rw;
   };
-  int unit = blockIdx.x;
-  Raw raw = load_raw(unit);
+  const int unit = blockIdx.x;
+  if (unit >= nunits) return;
+  const Raw raw = load_raw(unit);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // f^T comes from transpose_bm
-  for (; unit < nunits; unit += gridDim.x) {
   int y0, c0, qs;
   unit_geom(unit, y0, c0, qs);
   const int lo_c = c0 - M;
   const int lo0 = raw.c[0], len0 = raw.c[1] - raw.c[0], sh0 = -lo_c;
   const int lo1 = raw.c[2], len1 = raw.c[3] - raw.c[2], sh1 = lo_c < 0 ? -lo_c - NtL : NtL - lo_c;
-  raw = load_raw(unit + gridDim.x);
   int total;
   const int roff = warp_exclusive_scan(len0 + len1, total);
   int cs0 = c0 - (NtL >> 1);
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
       z.y = (T)0;
       grid[(long long)(b0 + bb) * g.grid_cells + (long long)ys * NtL + cs] = z;
     }
-    continue;
+    return;
   }
   // this warp's slice [vs, ve) of the virtual sequence
   const int vs = (int)(((long long)total * warp) / NW), ve = (int)(((long long)total * (warp + 1)) / NW);
@@ -484,8 +484,7 @@ __global__ void __launch_bounds__(32 * RB2_WARPS, NFFTB_RB2_MINB) spread_rb2_ker
       grid[(long long)(b0 + bb) * g.grid_cells + rowoff + cs] = a;
     }
   }
-  __syncthreads();  // the partials are consumed before the next unit stages into the same memory
-  }  // units
+
 }
 #undef NFFTB_RB2_STEP
 
