@@ -155,9 +155,15 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
 // A window with more than S1_CAP nodes is processed in chunks (the
 // accumulators stay in registers).
 constexpr int S1_THREADS = 128;
-constexpr int S1_K = 4;                   // consecutive cells per thread
+#ifndef NFFTB_S1_K
+#define NFFTB_S1_K 4
+#endif
+#ifndef NFFTB_S1_CAP
+#define NFFTB_S1_CAP 320
+#endif
+constexpr int S1_K = NFFTB_S1_K;          // consecutive cells per thread
 constexpr int S1_SEG = S1_THREADS * S1_K; // 512 cells per CTA
-constexpr int S1_CAP = 320;               // staged nodes per chunk (mean ~0.5 (SEG + 2m) at M = N = Nt/2)
+constexpr int S1_CAP = NFFTB_S1_CAP;      // staged nodes per chunk (mean ~0.5 (SEG + 2m) at M = N = Nt/2)
 // resident CTAs per SM of the spread launch (grid-stride over the segments, software-pipelined: the
 // next segment's loads overlap the current one's arithmetic). Measured on B200 (1D 2^18, m = 4): alone,
 // 4 per SM 10.5 us (3: 12.7, 2: 14.1); in the bench step with the direct NFFT running concurrently
