@@ -70,7 +70,7 @@ typedef enum {
   NFFT_METHOD_TILED = 1,  /* Alg. 3/4 over CELL-sorted nodes: interpolation per tile
                              with the tile + m-halo staged in shared memory; owner-computes adjoints
                              (D = 1 warp segments; D = 2, 3 warp-owned cell blocks over stored taps;
-                             2D batches of >= 8: row segments with lanes = vectors) */
+                             2D batches of >= 8: units of 2 rows x 16 cells, lanes = vectors) */
   NFFT_METHOD_DIRECT = 2, /* unblocked resampling straight from L2/HBM */
   NFFT_METHOD_TILED_CAS = 3, /* tiled; adjoint accumulates with shared-memory atomics (reference variant) */
   NFFT_METHOD_TILED_LOC = 4, /* tiled; adjoint lanes-own-cells + global reduction flush (D <= 2) */
@@ -252,7 +252,7 @@ nfft_status nfft_autotune_tile(int D, const int64_t* N, int64_t M, const void* n
 /* Paths the plan selected at creation (bit set = in use):
  *   NFFT_FEATURE_CELL_MODE   nodes sorted by cell, cell-mode resampling kernels
  *   NFFT_FEATURE_TENSOR      TENSOR precompute (stored taps)
- *   NFFT_FEATURE_BATCH       2D batch adjoint: row segments, lanes = batch vectors (B >= 8)
+ *   NFFT_FEATURE_BATCH       2D batch adjoint: units of output rows x cells, lanes = batch vectors (B >= 8)
  *   NFFT_FEATURE_WBLOCK      D = 2, 3 adjoint over warp-owned cell blocks and stored taps
  *   NFFT_FEATURE_FULL        FULL precompute (the sparse matrix B stored) */
 #define NFFT_FEATURE_CELL_MODE 1

@@ -584,10 +584,12 @@ def test_strategy_shards_sum_to_full_transform(precompute, D):
 
 
 @pytest.mark.parametrize("case", ["2d_c64_b32", "2d_c128_b9", "radial_b33_s125", "2d_c64_b8_m8"] +
-                         [f"2d_c128_b8_m{mm}" for mm in (1, 2, 5, 6, 7)] + [f"2d_c64_b16_m{mm}" for mm in (5, 6, 7)])
+                         [f"2d_c128_b8_m{mm}" for mm in (1, 2, 5, 6, 7)] + [f"2d_c64_b16_m{mm}" for mm in (1, 2, 3, 5, 6, 7)])
 def test_batch_adjoint(case):
-    """2D batches of >= 8 transforms: row-segment adjoint with lanes = batch
-    vectors (resample_rowbatch.cuh); every vector against the oracle, ragged
+    """2D batches of >= 8 transforms: the batch adjoint with lanes = batch
+    vectors (spread_rb2, resample_rowbatch.cuh) and, for fp32, the two-vector
+    interpolation (interp_cell2, bank-rotated for 2m = 8, 16); every vector
+    against the oracle, ragged
     chunks (B = 9, 33), wrapped windows, c64 and c128."""
     if case == "2d_c64_b32":
         w = workloads.make("cfg5_radial_s2", seed=13, N=(40, 36), M=1200, m=4, batch=32)
