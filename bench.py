@@ -516,7 +516,8 @@ def run_steps(a, ctx, w, mode, steps, warmup, staged=False, with_pre=False, seq_
     features = sorted(plan.features())
     obj.close()
     return dict(ms=float(ms_t.item()), stage=stage, launches=launches, clocks=clk.summary(),
-                units_total=units_total, features=features, median_ms=statistics.median(per_step))
+                units_total=units_total, features=features, median_ms=statistics.median(per_step),
+                midmean_ms=midmean(per_step))
 
 
 def roofline(w, means, step_ms, hbm, hbm_src, fp):
@@ -546,10 +547,21 @@ def roofline(w, means, step_ms, hbm, hbm_src, fp):
                  "algorithmic_bytes": bytes_of[dom], "algorithmic_flops": flops_of.get(dom, 0),
                  "kernel_ms_mean": means[dom], "kernel_share": means[dom] / step_ms,
                  "note": "kernel duration = marginal time of its stage in one graph of the seven stages run one "
-                         "after another (median sequence time minus the median of the sequence without the stage, "
+                         "after another (interquartile-mean sequence time minus that of the sequence without the stage, "
                          "L2 flushed before each step; D >= 2 spread stage includes the value permutation "
                          "kernel)"})
     return roof
+
+
+def midmean(xs):
+    """Interquartile mean. CUDA event differences on this box come in ~2 us
+    quanta, so a median of per-step times is quantised too; the mean over the
+    middle half averages the quanta (the event phases are random from step to
+    step) and still drops the flush-induced outliers."""
+    xs = sorted(xs)
+    k = len(xs) // 4
+    mid = xs[k:len(xs) - k] or xs
+    return sum(mid) / len(mid)
 
 
 def measure_config(a, ctx, config, mode, steps, warmup, m=None, e2e=True, cpu=True, extra=True, with_pre=True,
@@ -571,12 +583,13 @@ def measure_config(a, ctx, config, mode, steps, warmup, m=None, e2e=True, cpu=Tr
         out["stages_ms_mean"] = means
         out["ms_per_step_sequential"] = st["ms"] / n2
         # marginal stage times: the seven-stage sequence with and without each stage (no event nodes);
-        # medians of the per-step times (the flush before every step makes single steps noisy)
-        n3 = max(n2, 60)
-        full = run_steps(a, ctx, w, mode, n3, warmup, seq_omit=-1)["median_ms"]
+        # interquartile means of the per-step times (the flush before every step makes single steps
+        # noisy, and the event clock's ~2 us quantum would quantise a median)
+        n3 = max(n2, 100)
+        full = run_steps(a, ctx, w, mode, n3, warmup, seq_omit=-1)["midmean_ms"]
         marg = {}
         for k, name in enumerate(["precompute", "deconv", "fft_fwd", "interp", "spread", "fft_adj", "crop"]):
-            marg[name] = full - run_steps(a, ctx, w, mode, n3, warmup, seq_omit=k)["median_ms"]
+            marg[name] = full - run_steps(a, ctx, w, mode, n3, warmup, seq_omit=k)["midmean_ms"]
         out["stages_ms_marginal"] = marg
         out["ms_per_step_sequential_no_events"] = full
         if with_pre:

@@ -843,10 +843,16 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
     // no zero pass
     rec(p, 1, 1);
     // launch width: narrower when the direct NFFT runs concurrently (nfft_execute), resample1d.cuh
-    const unsigned segs = std::min<unsigned>((unsigned)((p->Nt[0] + S1_SEG - 1) / S1_SEG),
-                                             (unsigned)((overlap ? S1_CTAS_OVERLAP : S1_CTAS_ALONE) * p->sm_count));
+    // (alone: every segment its own CTA, the hardware refills the SMs; overlapped: a grid-stride launch
+    // of S1_CTAS_OVERLAP CTAs per SM, so the direct NFFT's kernels find room)
+    const bool stored = p->tensor || p->full;
+    const unsigned nsegs = (unsigned)((p->Nt[0] + S1_SEG - 1) / S1_SEG);
+    const unsigned width = (overlap ? S1_CTAS_OVERLAP : S1_CTAS_ALONE) > 0
+                               ? (unsigned)((overlap ? S1_CTAS_OVERLAP : S1_CTAS_ALONE) * p->sm_count)
+                               : nsegs;
+    const unsigned segs = std::min(nsegs, width);
     // FULL in 1D: the rows of B are the 2m taps, so the TENSOR kernel reads them
-    CK(launch_k((p->tensor || p->full) ? ks.spread1t : ks.spread1, dim3(segs, (unsigned)p->B), S1_THREADS,
+    CK(launch_k(stored ? ks.spread1t : ks.spread1, dim3(segs, (unsigned)p->B), S1_THREADS,
                 p->r1_spread_bytes, st, p->geom, WpnArg{p->wpn}, f, (const T*)p->d_kc,
                 (const T*)(p->full ? p->d_bw : p->d_wt), (const int*)p->d_jc,
                 (const int*)p->d_cstart, p->node_begin, p->node_end, grid));

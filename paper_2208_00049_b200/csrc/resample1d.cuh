@@ -154,7 +154,10 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
 //     reading the halo NODES).
 // A window with more than S1_CAP nodes is processed in chunks (the
 // accumulators stay in registers).
-constexpr int S1_THREADS = 128;
+#ifndef NFFTB_S1_THREADS
+#define NFFTB_S1_THREADS 128
+#endif
+constexpr int S1_THREADS = NFFTB_S1_THREADS;
 #ifndef NFFTB_S1_K
 #define NFFTB_S1_K 4
 #endif
@@ -164,16 +167,17 @@ constexpr int S1_THREADS = 128;
 constexpr int S1_K = NFFTB_S1_K;          // consecutive cells per thread
 constexpr int S1_SEG = S1_THREADS * S1_K; // 512 cells per CTA
 constexpr int S1_CAP = NFFTB_S1_CAP;      // staged nodes per chunk (mean ~0.5 (SEG + 2m) at M = N = Nt/2)
-// resident CTAs per SM of the spread launch (grid-stride over the segments, software-pipelined: the
-// next segment's loads overlap the current one's arithmetic). Measured on B200 (1D 2^18, m = 4): alone,
-// 4 per SM 10.5 us (3: 12.7, 2: 14.1); in the bench step with the direct NFFT running concurrently
-// (nfft_execute) the 121-register kernel at 4 per SM fills the register file and keeps the forward
-// FFT off the SMs (step 53.1 us), 3 per SM leaves it room (45.0 us). Hence two launch widths.
+// Launch width. Alone (nfft_adjoint): one CTA per segment, 4 resident per SM (104 registers) and the
+// hardware refills the SMs as CTAs retire: 1D 2^18, m = 4 11.5-12 us where the round-2 software
+// pipeline (138 registers, 3 CTAs/SM) took 14.3 us on the same box. Under nfft_execute, with the
+// direct NFFT running concurrently: a grid-stride launch of 4 CTAs per SM, so the pending CTAs of a
+// full-width launch do not take every freed slot ahead of the forward FFT (one CTA per segment there:
+// step 47-48 us vs 43.1 us).
 #ifndef NFFTB_S1_ALONE
-#define NFFTB_S1_ALONE 4
+#define NFFTB_S1_ALONE 0  // 0: one CTA per segment
 #endif
 #ifndef NFFTB_S1_OVERLAP
-#define NFFTB_S1_OVERLAP 3
+#define NFFTB_S1_OVERLAP 4
 #endif
 #ifndef NFFTB_S1_MINB
 #define NFFTB_S1_MINB 1
@@ -304,19 +308,17 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
   };
   int sgi = blockIdx.x;
   if (sgi >= nsegs) return;
-  // software pipeline over this CTA's segments (grid-stride): the next segment's window bounds are
-  // loaded while the current one is staged, its nodes' coordinates / indices while it is gathered and
-  // their values right after, so its load chain overlaps the current segment's arithmetic
-  Meta mc = load_meta(sgi);
-  Batch bc, bn;
-  load_nodes(mc, 0, bc);
-  load_vals(bc);
-  NFFTB_TRACE(1);
+  // One segment after another (a launch alone has one CTA per segment and the hardware refills the
+  // SMs; under nfft_execute the launch is narrower and the CTAs grid-stride). A software pipeline over
+  // the CTA's segments (next segment's loads during the gather: 138 registers, 3 CTAs/SM) and an L2
+  // prefetch of the successor segment's load chain were measured slower / neutral
+  // (attic/spread1s_pipeline_and_l2_prefetch.diff.txt).
   while (true) {
-    const int sn = sgi + gridDim.x;
-    const bool has_next = sn < nsegs;
-    Meta mn;
-    if (has_next) mn = load_meta(sn);
+    const Meta mc = load_meta(sgi);
+    Batch bc;
+    load_nodes(mc, 0, bc);
+    load_vals(bc);
+    NFFTB_TRACE(1);
     C acc[S1_K];
 #pragma unroll
     for (int k = 0; k < S1_K; ++k) {
@@ -334,9 +336,6 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
       NFFTB_TRACE(2);
       __syncthreads();
       NFFTB_TRACE(3);
-      if (clo == 0 && has_next) load_nodes(mn, 0, bn);
-      // 3. owner-computes gather: node in window cell K t + v adds to cell K t + k with tap
-      //    l = k - v + 2m - 1 when 0 <= l < 2m
       const int lo = max(mc.r_lo - clo, 0), hi = min(mc.r_hi - clo, cnt);
       for (int q = lo; q < hi; ++q) {
         const C val = sval[q];
@@ -353,9 +352,7 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
         }
       }
     }
-    if (has_next) load_vals(bn);
     NFFTB_TRACE(4);
-    // 4. one plain store per owned cell (binning cell y <-> storage (y - Nt/2) mod Nt)
     C* dst = grid + (long long)b * g.grid_cells;
     int s = mc.y0 + S1_K * t - (Nt >> 1);
     if (s < 0) s += Nt;
@@ -367,11 +364,9 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
         dst[sk] = acc[k];
       }
     }
-    if (!has_next) break;
+    sgi += gridDim.x;
+    if (sgi >= nsegs) break;
     __syncthreads();  // the gathers of this segment are done before the next one is staged
-    sgi = sn;
-    mc = mn;
-    bc = bn;
   }
 }
 

@@ -179,6 +179,14 @@ static void run(int M_nodes, int Nt) {
       printf("%s{\"slot\": %d, \"min\": %.2f, \"p10\": %.2f, \"p50\": %.2f, \"p90\": %.2f, \"max\": %.2f}", s ? ", " : "", s, v[0],
              v[v.size() / 10], v[v.size() / 2], v[v.size() * 9 / 10], v.back());
     }
+    printf("], \"durations\": [");
+    for (int s = 1; s < nslots; ++s) {  // per-CTA phase durations (slot s - slot s-1)
+      std::vector<double> v;
+      for (unsigned c = 0; c < nctas; ++c) v.push_back(((double)keep[c * 8 + s] - (double)keep[c * 8 + s - 1]) * 1e-3);
+      std::sort(v.begin(), v.end());
+      printf("%s{\"phase\": %d, \"p10\": %.2f, \"p50\": %.2f, \"p90\": %.2f, \"max\": %.2f}", s > 1 ? ", " : "", s,
+             v[v.size() / 10], v[v.size() / 2], v[v.size() * 9 / 10], v.back());
+    }
     printf("]}\n");
   }
   cudaFree(d_kc);
