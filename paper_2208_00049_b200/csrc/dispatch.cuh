@@ -93,9 +93,9 @@ KernelSet<T> make_set() {
   if constexpr (D == 1) {
     k.interp1 = (const void*)interp1s_kernel<T, M, DEG, false>;
     k.interp1t = (const void*)interp1s_kernel<T, M, DEG, true>;
-    k.spread1 = (const void*)spread1s_kernel<T, M, DEG, false>;
+    k.spread1 = (const void*)spread1a_kernel<T, M, DEG, false>;
     k.taps1 = (const void*)taps1_kernel<T, M, DEG>;
-    k.spread1t = (const void*)spread1s_kernel<T, M, DEG, true>;
+    k.spread1t = (const void*)spread1a_kernel<T, M, DEG, true>;
   } else {
     k.interp_cell = (const void*)interp_cell_kernel<T, D, M, DEG, false>;
     k.interp_cellt = (const void*)interp_cell_kernel<T, D, M, DEG, true>;

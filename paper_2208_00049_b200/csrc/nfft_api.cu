@@ -92,7 +92,7 @@ struct nfft_plan_s {
   bool cellmode = false;
   bool tile_binned = false;  // cell mode: perm/offsets (tile sort) computed on demand for nfft_get_binning
   int64_t ncells = 0;        // prod Ntilde
-  size_t r1_spread_bytes = 0; // spread1s shared memory
+  size_t r1_spread_bytes = 0; // spread1a shared memory
   size_t r1_interp_bytes = 0; // interp1s shared memory
   size_t sc_bytes = 0;       // spread_cell shared memory
   int sc_cap = 0;            // spread_cell node slots per chunk

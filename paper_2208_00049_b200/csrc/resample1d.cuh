@@ -4,24 +4,19 @@
 //   forward: f_j = sum_l ghat_l psi~(k_j - l/Nt)        (Alg. 3)
 //   adjoint: ghat_l = sum_j f_j psi~(k_j - l/Nt)         (Alg. 4)
 //
-// cellsort1d (precompute, one warp per tile): refines the stable tile sort of
-//   binsort.cuh to the stable CELL order inside each tile (in 1D the tiles are
-//   consecutive cell ranges, so this is the global cell order) and writes the
-//   cell offset table cstart[c] (first cell-sorted position of cell c). It is
-//   computed once per node set and shared by every forward and adjoint.
-// interp1c: one thread per node in cell order; the 2m grid cells are read
-//   straight from L2 (the FFT output is L2-resident): consecutive lanes hold
-//   nodes of nearby cells, so their windows overlap in L1. No staging, no
-//   barrier, one dependent load level before the arithmetic.
-// spread1c: OWNER-COMPUTES gather, one warp per 32 K consecutive cells. The
-//   nodes that reach the warp's cells are the contiguous cell-sorted range of
-//   cells [y0 - m, y0 + 32K + m - 2] (the cstart table gives it, wrap included);
-//   the warp evaluates their taps once into shared memory and every lane sums,
-//   for each of its K cells y, f_j w_j[y - x_j + m - 1] over the contiguous slot
-//   range of cells x in [y - m, y + m - 1]. Every cell is written exactly once
-//   with a plain coalesced store: no atomics, no zero pass, no halo merge (the
-//   paper's locked merge of PAPER.md:578-582 disappears because the halo NODES
-//   are read instead of halo CELLS being reduced).
+// The nodes are in stable CELL order (cellbin.cuh: kc = coordinates, jc = the
+// caller's indices, cstart[c] = first cell-sorted position of cell c), computed
+// once per node set and shared by every forward and adjoint.
+// interp1s: one CTA per segment of 512 cells, the paper's block with its index
+//   set cached in shared memory (Alg. 3).
+// spread1a: OWNER-COMPUTES gather, one CTA per segment: the nodes that reach the
+//   segment's cells are ONE contiguous cell-sorted range (the cells' own nodes
+//   plus the halo NODES of the 2m - 1 neighbouring cells), staged once with
+//   their taps; every thread sums its 4 cells over the nodes in reach and every
+//   cell is written exactly once with a plain coalesced store: no atomics, no
+//   zero pass, no halo merge (the paper's locked merge of PAPER.md:578-582
+//   disappears because the halo NODES are read instead of halo CELLS being
+//   reduced).
 #pragma once
 
 #include "resample.cuh"
@@ -133,7 +128,7 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
 }
 
 // ---------------------------------------------------------------- adjoint
-// spread1s: OWNER-COMPUTES gather, one CTA per segment of S1_SEG consecutive
+// spread1a: OWNER-COMPUTES gather, one CTA per segment of S1_SEG consecutive
 // cells (b = blockIdx.y). The nodes that reach the segment are those of the
 // window cells [y0 - m, y0 + SEG + m - 2]: ONE contiguous range of the
 // cell-sorted order (cstart; a wrapped window is a wrapped range, handled with
@@ -149,9 +144,7 @@ __global__ void __launch_bounds__(I1_THREADS) interp1s_kernel(Geom g, WinPolyN<T
 //     walk is one loop without per-cell divergence); a node in window cell x
 //     adds f_j w_j[y - x + m - 1] to every owned cell y in its reach
 //     (predicated loads and FMAs, no branches),
-//  4. writes each of its cells once (plain stores: no atomics, no zero pass,
-//     no halo merge — the paper's locked merge of PAPER.md:578-582 becomes
-//     reading the halo NODES).
+//  4. writes each of its cells once.
 // A window with more than S1_CAP nodes is processed in chunks (the
 // accumulators stay in registers).
 #ifndef NFFTB_S1_THREADS
@@ -167,20 +160,15 @@ constexpr int S1_THREADS = NFFTB_S1_THREADS;
 constexpr int S1_K = NFFTB_S1_K;          // consecutive cells per thread
 constexpr int S1_SEG = S1_THREADS * S1_K; // 512 cells per CTA
 constexpr int S1_CAP = NFFTB_S1_CAP;      // staged nodes per chunk (mean ~0.5 (SEG + 2m) at M = N = Nt/2)
-// Launch width. Alone (nfft_adjoint): one CTA per segment, 4 resident per SM (104 registers) and the
-// hardware refills the SMs as CTAs retire: 1D 2^18, m = 4 11.5-12 us where the round-2 software
-// pipeline (138 registers, 3 CTAs/SM) took 14.3 us on the same box. Under nfft_execute, with the
-// direct NFFT running concurrently: a grid-stride launch of 4 CTAs per SM, so the pending CTAs of a
-// full-width launch do not take every freed slot ahead of the forward FFT (one CTA per segment there:
-// step 47-48 us vs 43.1 us).
+// Launch width. Alone (nfft_adjoint): one CTA per segment; 7 CTAs per SM are resident, so the 1024
+// segments of the headline configuration (1D 2^18, sigma = 2) run as one wave. Under nfft_execute,
+// with the direct NFFT running concurrently: a grid-stride launch of S1_CTAS_OVERLAP CTAs per SM, so
+// the forward FFT finds room (one CTA per segment there: step 50 us vs 42.6-43.3 us).
 #ifndef NFFTB_S1_ALONE
 #define NFFTB_S1_ALONE 0  // 0: one CTA per segment
 #endif
 #ifndef NFFTB_S1_OVERLAP
-#define NFFTB_S1_OVERLAP 4
-#endif
-#ifndef NFFTB_S1_MINB
-#define NFFTB_S1_MINB 1
+#define NFFTB_S1_OVERLAP 5
 #endif
 constexpr int S1_CTAS_ALONE = NFFTB_S1_ALONE;
 constexpr int S1_CTAS_OVERLAP = NFFTB_S1_OVERLAP;
@@ -188,7 +176,7 @@ constexpr int S1_CTAS_OVERLAP = NFFTB_S1_OVERLAP;
 // tap row pitch: 2m taps, odd pitch (neighbouring rows in distinct banks)
 __host__ __device__ constexpr int s1_pitch(int M) { return 2 * M + 1; }
 
-// shared memory of one spread1s CTA (host and device agree)
+// shared memory of one spread1a CTA (host and device agree)
 __host__ __device__ inline size_t s1_smem_bytes(int M, size_t csize, size_t rsize) {
   size_t b = (size_t)S1_CAP * csize;                       // staged values
   b += (size_t)S1_CAP * s1_pitch(M) * rsize;               // staged tap rows
@@ -197,8 +185,37 @@ __host__ __device__ inline size_t s1_smem_bytes(int M, size_t csize, size_t rsiz
   return (b + 15) & ~(size_t)15;
 }
 
+// The load chain is staged through shared memory by cp.async instead of through registers. The
+// round-2 kernel (attic/spread1s_register_staged.cuh.txt) kept a thread's three window nodes
+// (coordinate, index, wrap, value) in registers across the two dependent load levels: 104 registers,
+// 4 CTAs per SM, so the 1024 segments of 2^19 cells ran as two waves of ~6 us each
+// (tools/micro/trace1d.cu). Here
+//   level 1  cstart -> the window's node range and this thread's reach (registers, as before),
+//   level 2  coordinates and indices: cp.async into the slots they will be overwritten in (the
+//            coordinate into the node's tap row, the index into its window-cell slot),
+//   level 3  values f[jc]: cp.async gather straight into the staged-value array, in flight while the
+//            thread evaluates its nodes' taps one node at a time,
+// so no node state lives in registers across a load level, the kernel fits S1A_MINB CTAs per SM and
+// every segment of the headline configuration is resident at once (one wave). A thread waits only
+// on its own copies before it reads them (cp.async.wait_group), the CTA barrier comes once, before
+// the gather.
+#ifndef NFFTB_S1A_MINB
+#define NFFTB_S1A_MINB 7
+#endif
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_n(void* sdst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+  else if constexpr (BYTES == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
 template <typename T, int M, int DEG, bool TENSOR>
-__global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geom g, WinPolyN<T, 1, M> wp,
+__global__ void __launch_bounds__(S1_THREADS, NFFTB_S1A_MINB) spread1a_kernel(Geom g, WinPolyN<T, 1, M> wp,
                                                               const typename cplx<T>::type* __restrict__ f,
                                                               const T* __restrict__ kc, const T* __restrict__ wt,
                                                               const int* __restrict__ jc,
@@ -206,7 +223,6 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
                                                               typename cplx<T>::type* __restrict__ grid) {
   using C = typename cplx<T>::type;
   constexpr int TAPS = 2 * M, TP = s1_pitch(M), REACH = S1_K + 2 * M - 1;
-  constexpr int U = (S1_CAP + S1_THREADS - 1) / S1_THREADS;  // staged nodes per thread and chunk
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* sval = reinterpret_cast<C*>(smem_raw);
   T* stap = reinterpret_cast<T*>(sval + S1_CAP);
@@ -217,18 +233,12 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
   const int nsegs = (Nt + S1_SEG - 1) / S1_SEG;
   const int t = threadIdx.x;
   const C* fb = f + (long long)b * Mn;
-  // 1. a segment's window: node range (virtual positions, uniform) and this thread's reach, window
-  //    cells [K t, K t + REACH); virtual position of window cell u: cstart[c mod Nt] + M floor(c / Nt)
-  struct Meta {
-    int y0, nseg, vbase, total, r_lo, r_hi;
-  };
-  auto load_meta = [&](int sgi) {
-    Meta mt;
-    mt.y0 = sgi * S1_SEG;
-    mt.nseg = min(S1_SEG, Nt - mt.y0);
-    const int W = mt.nseg + 2 * M - 1;  // window cell u <-> binning cell y0 - m + u
+  for (int sgi = blockIdx.x; sgi < nsegs; sgi += gridDim.x) {
+    // level 1: the window's node range (virtual positions) and this thread's reach
+    const int y0 = sgi * S1_SEG, nseg = min(S1_SEG, Nt - y0);
+    const int W = nseg + 2 * M - 1;  // window cell u <-> binning cell y0 - m + u
     auto vpos = [&](int u) {
-      int c = mt.y0 - M + u, wrap = 0;  // c in (-Nt, 2 Nt): 2m < Nt
+      int c = y0 - M + u, wrap = 0;  // c in (-Nt, 2 Nt): 2m < Nt
       if (c < 0) {
         c += Nt;
         wrap = -1;
@@ -238,105 +248,75 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
       }
       return __ldg(cstart + c) + wrap * Mn;
     };
-    mt.vbase = vpos(0);
-    mt.total = vpos(W) - mt.vbase;
-    mt.r_lo = vpos(min(S1_K * t, W)) - mt.vbase;
-    mt.r_hi = vpos(min(S1_K * t + REACH, W)) - mt.vbase;
-    return mt;
-  };
-  // 2. a chunk's nodes: coordinates and indices (first load level), then the values (second level)
-  struct Batch {
-    int pp[U], jj[U], wv[U];
-    double kk[U];
-    C v[U];
-  };
-  auto load_nodes = [&](const Meta& mt, int clo, Batch& bt) {
-    const int cnt = min(S1_CAP, mt.total - clo);
-#pragma unroll
-    for (int i = 0; i < U; ++i) {
-      const int q = t + i * S1_THREADS;
-      bt.pp[i] = -1;
-      bt.jj[i] = -1;
-      bt.wv[i] = 0;
-      bt.kk[i] = 0.0;
-      if (q < cnt) {
-        int p = mt.vbase + clo + q;  // virtual position in (-M, 2M)
-        if (p < 0) {
-          p += Mn;
-          bt.wv[i] = -1;
-        } else if (p >= Mn) {
-          p -= Mn;
-          bt.wv[i] = 1;
-        }
-        bt.pp[i] = p;
-        bt.kk[i] = (double)kc[p];
-        bt.jj[i] = (p >= nb && p < ne) ? __ldg(jc + p) : -1;  // node shard = range [nb, ne) of the cell order
-      }
-    }
-  };
-  auto load_vals = [&](Batch& bt) {
-#pragma unroll
-    for (int i = 0; i < U; ++i) {
-      bt.v[i].x = (T)0;
-      bt.v[i].y = (T)0;
-      if (bt.jj[i] >= 0) bt.v[i] = fb[bt.jj[i]];
-    }
-  };
-  // stage: taps (from the coordinates, or the TENSOR table), window cell and value of every node
-  auto stage = [&](const Meta& mt, const Batch& bt) {
-#pragma unroll
-    for (int i = 0; i < U; ++i) {
-      const int q = t + i * S1_THREADS;
-      if (bt.pp[i] < 0) continue;
-      double frac;
-      const int c = node_cell(bt.kk[i], g.Ntd[0], Nt, frac);
-      scel[q] = c + bt.wv[i] * Nt - (mt.y0 - M);  // window cell (virtual cell of the virtual position)
-      T w[TAPS];
-      if constexpr (TENSOR) {
-#pragma unroll
-        for (int l = 0; l < TAPS; ++l) w[l] = __ldg(wt + (long long)bt.pp[i] * TAPS + l);
-      } else {
-        window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
-      }
-      T* row = stap + q * TP;
-#pragma unroll
-      for (int l = 0; l < TAPS; ++l) row[l] = w[l];
-    }
-#pragma unroll
-    for (int i = 0; i < U; ++i)
-      if (bt.pp[i] >= 0) sval[t + i * S1_THREADS] = bt.v[i];
-  };
-  int sgi = blockIdx.x;
-  if (sgi >= nsegs) return;
-  // One segment after another (a launch alone has one CTA per segment and the hardware refills the
-  // SMs; under nfft_execute the launch is narrower and the CTAs grid-stride). A software pipeline over
-  // the CTA's segments (next segment's loads during the gather: 138 registers, 3 CTAs/SM) and an L2
-  // prefetch of the successor segment's load chain were measured slower / neutral
-  // (attic/spread1s_pipeline_and_l2_prefetch.diff.txt).
-  while (true) {
-    const Meta mc = load_meta(sgi);
-    Batch bc;
-    load_nodes(mc, 0, bc);
-    load_vals(bc);
-    NFFTB_TRACE(1);
+    const int vbase = vpos(0);
+    const int total = vpos(W) - vbase;
+    const int r_lo = vpos(min(S1_K * t, W)) - vbase;
+    const int r_hi = vpos(min(S1_K * t + REACH, W)) - vbase;
     C acc[S1_K];
 #pragma unroll
     for (int k = 0; k < S1_K; ++k) {
       acc[k].x = (T)0;
       acc[k].y = (T)0;
     }
-    for (int clo = 0; clo < mc.total; clo += S1_CAP) {
-      const int cnt = min(S1_CAP, mc.total - clo);
-      if (clo > 0) {  // a dense window: further chunks are loaded in place
-        __syncthreads();
-        load_nodes(mc, clo, bc);
-        load_vals(bc);
+    for (int clo = 0; clo < total; clo += S1_CAP) {
+      const int cnt = min(S1_CAP, total - clo);
+      // level 2: coordinates -> first element of the node's tap row, indices -> its window-cell slot
+      for (int q = t; q < cnt; q += S1_THREADS) {
+        int p = vbase + clo + q;  // virtual position in (-M, 2M)
+        if (p < 0) p += Mn;
+        else if (p >= Mn) p -= Mn;
+        cp_async_n<sizeof(T)>(stap + q * TP, kc + p);
+        cp_async_n<4>(scel + q, jc + p);
       }
-      stage(mc, bc);
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+      // level 3: values -> staged values (node shard = range [nb, ne) of the cell order; others add 0)
+      for (int q = t; q < cnt; q += S1_THREADS) {
+        int p = vbase + clo + q;
+        if (p < 0) p += Mn;
+        else if (p >= Mn) p -= Mn;
+        if (p >= nb && p < ne) {
+          cp_async_n<sizeof(C)>(sval + q, fb + scel[q]);
+        } else {
+          C z;
+          z.x = (T)0;
+          z.y = (T)0;
+          sval[q] = z;
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      NFFTB_TRACE(1);
+      // taps (from the coordinates, or the TENSOR table) and window cells, one node at a time
+#pragma unroll 1
+      for (int q = t; q < cnt; q += S1_THREADS) {
+        int p = vbase + clo + q, wv = 0;
+        if (p < 0) {
+          p += Mn;
+          wv = -1;
+        } else if (p >= Mn) {
+          p -= Mn;
+          wv = 1;
+        }
+        T* row = stap + q * TP;
+        double frac;
+        const int c = node_cell((double)row[0], g.Ntd[0], Nt, frac);
+        scel[q] = c + wv * Nt - (y0 - M);  // window cell (virtual cell of the virtual position)
+        T w[TAPS];
+        if constexpr (TENSOR) {
+#pragma unroll
+          for (int l = 0; l < TAPS; ++l) w[l] = __ldg(wt + (long long)p * TAPS + l);
+        } else {
+          window_taps<T, M, DEG>((T)(frac - 0.5), wp.mu[0], w);
+        }
+#pragma unroll
+        for (int l = 0; l < TAPS; ++l) row[l] = w[l];
+      }
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       NFFTB_TRACE(2);
       __syncthreads();
       NFFTB_TRACE(3);
-      const int lo = max(mc.r_lo - clo, 0), hi = min(mc.r_hi - clo, cnt);
+      // owner-computes gather: node in window cell K t + v adds to cell K t + k with tap
+      // l = k - v + 2m - 1 when 0 <= l < 2m
+      const int lo = max(r_lo - clo, 0), hi = min(r_hi - clo, cnt);
       for (int q = lo; q < hi; ++q) {
         const C val = sval[q];
         const int l0 = TAPS - 1 - (scel[q] - S1_K * t);
@@ -351,22 +331,21 @@ __global__ void __launch_bounds__(S1_THREADS, NFFTB_S1_MINB) spread1s_kernel(Geo
           }
         }
       }
+      __syncthreads();  // the gathers are done before the next chunk / segment is staged
     }
     NFFTB_TRACE(4);
+    // one plain store per owned cell (binning cell y <-> storage (y - Nt/2) mod Nt)
     C* dst = grid + (long long)b * g.grid_cells;
-    int s = mc.y0 + S1_K * t - (Nt >> 1);
+    int s = y0 + S1_K * t - (Nt >> 1);
     if (s < 0) s += Nt;
 #pragma unroll
     for (int k = 0; k < S1_K; ++k) {
-      if (S1_K * t + k < mc.nseg) {
+      if (S1_K * t + k < nseg) {
         int sk = s + k;
         if (sk >= Nt) sk -= Nt;
         dst[sk] = acc[k];
       }
     }
-    sgi += gridDim.x;
-    if (sgi >= nsegs) break;
-    __syncthreads();  // the gathers of this segment are done before the next one is staged
   }
 }
 

@@ -20,7 +20,7 @@
 // full_interp (forward): LPN lanes per node (8 for E <= 16, else 32) stride
 //   over the node's row (coalesced weight / index reads), reduce with
 //   shuffles, one store f[j].
-// full_spread (adjoint, D >= 2; D = 1 uses spread1s over the weights, which
+// full_spread (adjoint, D >= 2; D = 1 uses spread1a over the weights, which
 //   are then the taps): OWNER-COMPUTES, one thread per oversampled cell y: the
 //   nodes that reach y lie in the (2m)^(D-1) rows of the footprint box, each a
 //   contiguous cell-sorted range along the last dimension (two where it

@@ -421,6 +421,42 @@ def test_execute_overlapped_matches_oracle(D):
     plan.close()
 
 
+@pytest.mark.parametrize("config", ["cfg2_1d_2e18", "cfg3_2d_512", "cfg4_3d_64"])
+def test_full_size_execute_as_benched(config):
+    """The call bench.py times: one nfft_execute of the direct and the adjoint
+    NFFT (adjoint || forward; the 1D adjoint then runs its narrower grid-stride
+    launch, several segments per CTA), captured into a CUDA graph and replayed,
+    at BASELINE configs[1..3]' full size, against the oracle."""
+    torch = _torch()
+    import paper_2208_00049_b200 as pkg
+    w = workloads.make(config, seed=3)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        plan = pkg.NfftPlan(torch.from_numpy(w["nodes"]).cuda(), w["N"], m=w["m"], sigma=w["sigma"],
+                            stream=st.cuda_stream).precompute()
+        fhat = torch.from_numpy(w["fhat"]).cuda()
+        f = torch.from_numpy(w["f"]).cuda()
+        fo = torch.empty((1, w["M"]), dtype=torch.complex128, device="cuda")
+        yo = torch.empty((1,) + tuple(w["N"]), dtype=torch.complex128, device="cuda")
+        plan.execute(False, fhat, fo, f, yo)
+    st.synchronize()
+    rf, ry = _oracle(w)
+    assert rel_l2(fo.cpu().numpy()[0], rf[0]) <= 1e-12
+    assert rel_l2(yo.cpu().numpy()[0], ry[0]) <= 1e-12
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        plan.execute(False, fhat, fo, f, yo)
+    for _ in range(3):  # replays reuse the plan's grids (the adjoint grid must come back zeroed)
+        fo.zero_()
+        yo.zero_()
+        with torch.cuda.stream(st):
+            g.replay()
+        st.synchronize()
+        assert rel_l2(fo.cpu().numpy()[0], rf[0]) <= 1e-12
+        assert rel_l2(yo.cpu().numpy()[0], ry[0]) <= 1e-12
+    plan.close()
+
+
 # ------------------------------------------------------------------ D = 1 static-tile path + one-kernel sort
 
 @pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])

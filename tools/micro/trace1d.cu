@@ -9,6 +9,7 @@
 //        -I include -o /tmp/trace1d tools/micro/trace1d.cu && /tmp/trace1d [m]
 #define NFFTB_PHASE_TRACE
 #include "../../paper_2208_00049_b200/csrc/resample1d.cuh"
+#define SPREAD1 spread1a_kernel
 
 #include <algorithm>
 #include <cmath>
@@ -89,7 +90,7 @@ static void run(int M_nodes, int Nt) {
   const size_t FL = 512ull << 20;
   cudaMalloc(&flush, FL);
   const size_t sb = s1_smem_bytes(M, 16, 8), ib = i1_smem_bytes(M, 16);
-  cudaFuncSetAttribute((const void*)spread1s_kernel<double, M, DEG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+  cudaFuncSetAttribute((const void*)SPREAD1<double, M, DEG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
   cudaFuncSetAttribute((const void*)interp1s_kernel<double, M, DEG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ib);
   const unsigned segs_s = std::min<unsigned>((Nt + S1_SEG - 1) / S1_SEG, g_s1cap ? g_s1cap * 148 : 1u << 30), segs_i = (Nt + I1_SEG - 1) / I1_SEG;
   cudaEvent_t e0, e1;
@@ -109,7 +110,7 @@ static void run(int M_nodes, int Nt) {
       return ms * 1e3f / 20;
     };
     const float ts = b2b([&] {
-      spread1s_kernel<double, M, DEG, false><<<dim3(segs_s, 1), S1_THREADS, sb, st>>>(g, wp, d_f, d_kc, d_wt, d_jc, d_cs, 0,
+      SPREAD1<double, M, DEG, false><<<dim3(segs_s, 1), S1_THREADS, sb, st>>>(g, wp, d_f, d_kc, d_wt, d_jc, d_cs, 0,
                                                                                     M_nodes, d_grid);
     });
     const float ti = b2b([&] {
@@ -131,7 +132,7 @@ static void run(int M_nodes, int Nt) {
     cudaGraphExec_t ge;
     cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
     for (int i = 0; i < 20; ++i)
-      spread1s_kernel<double, M, DEG, false><<<dim3(segs_s, 1), S1_THREADS, sb, st>>>(g, wp, d_f, d_kc, d_wt, d_jc, d_cs, 0,
+      SPREAD1<double, M, DEG, false><<<dim3(segs_s, 1), S1_THREADS, sb, st>>>(g, wp, d_f, d_kc, d_wt, d_jc, d_cs, 0,
                                                                                     M_nodes, d_grid);
     cudaStreamEndCapture(st, &gr);
     cudaGraphInstantiate(&ge, gr, 0);
@@ -152,7 +153,7 @@ static void run(int M_nodes, int Nt) {
       cudaMemcpyToSymbol(nfftb_trace, tr.data(), 0);  // no-op, keeps symbol referenced
       cudaEventRecord(e0);
       if (which == 0)
-        spread1s_kernel<double, M, DEG, false><<<dim3(segs_s, 1), S1_THREADS, sb>>>(g, wp, d_f, d_kc, d_wt, d_jc, d_cs, 0,
+        SPREAD1<double, M, DEG, false><<<dim3(segs_s, 1), S1_THREADS, sb>>>(g, wp, d_f, d_kc, d_wt, d_jc, d_cs, 0,
                                                                                    M_nodes, d_grid);
       else
         interp1s_kernel<double, M, DEG, false><<<dim3(segs_i, 1), I1_THREADS, ib>>>(g, wp, d_grid, d_kc, d_wt, d_jc, d_cs, 0, M_nodes,
