@@ -33,7 +33,7 @@ __global__ void permute_scatter(const double2* __restrict__ f, const int* __rest
   if (j < M) fc[inv[j]] = f[j];
 }
 static bool g_flush = true;
-static unsigned g_s1cap = 0;  // spread1s CTAs per SM (0: one per segment); env S1CAP  // L2 flush before every launch (argv[2] = "warm": no flush)
+static unsigned g_s1cap = 0;  // spread1a CTAs per SM (0: one per segment); env S1CAP  // L2 flush before every launch (argv[2] = "warm": no flush)
 
 template <int M>
 static void run(int M_nodes, int Nt) {
@@ -137,7 +137,7 @@ static void run(int M_nodes, int Nt) {
     cudaStreamEndCapture(st, &gr);
     cudaGraphInstantiate(&ge, gr, 0);
     const float tg = b2b([&] { cudaGraphLaunch(ge, st); }) / 20;
-    printf("{\"b2b_us\": {\"spread1s\": %.2f, \"interp1s\": %.2f, \"spread1s_graph\": %.2f, \"empty_1024x128_bigparams\": %.2f, "
+    printf("{\"b2b_us\": {\"spread1a\": %.2f, \"interp1s\": %.2f, \"spread1a_graph\": %.2f, \"empty_1024x128_bigparams\": %.2f, "
            "\"empty_1024x128\": %.2f, \"empty_1x32\": %.2f, \"permute_scatter\": %.2f}}\n", ts, ti, tg, te, tes, tes1, tperm);
   }
   for (int which = 0; which < 2; ++which) {
@@ -171,7 +171,7 @@ static void run(int M_nodes, int Nt) {
     const int nslots = which == 0 ? 5 : 3;
     unsigned long long t0 = ~0ull;
     for (unsigned c = 0; c < nctas; ++c) t0 = std::min(t0, keep[c * 8 + 0]);
-    printf("{\"l2\": \"%s\", \"kernel\": \"%s\", \"m\": %d, \"ctas\": %u, \"event_us\": %.2f, \"phases\": [", g_flush ? "flushed" : "warm", which == 0 ? "spread1s" : "interp1s",
+    printf("{\"l2\": \"%s\", \"kernel\": \"%s\", \"m\": %d, \"ctas\": %u, \"event_us\": %.2f, \"phases\": [", g_flush ? "flushed" : "warm", which == 0 ? "spread1a" : "interp1s",
            M, nctas, best * 1e3);
     for (int s = 0; s < nslots; ++s) {
       std::vector<double> v;
