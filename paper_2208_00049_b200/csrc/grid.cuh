@@ -167,6 +167,8 @@ __global__ void __launch_bounds__(THREADS) correct_flat_kernel(Geom g, const typ
   const int hp = (nl + 1) >> 1;  // cell pairs per row
   const int units = (int)((long long)g.B * (g.ngrid_cells / nl)) * hp;
   const T* bl = beta + g.beta_off[D - 1];
+  // the crop may be launched programmatically after the inverse FFT (stage_crop, pdl): wait for the grid
+  if constexpr (!FWD) asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int u = blockIdx.x * THREADS + threadIdx.x; u < units; u += gridDim.x * THREADS) {
     const int row = u / hp;
     const int x0 = (u - row * hp) * 2;

@@ -891,8 +891,10 @@ nfft_status stage_spread(nfft_plan p, const typename cplx<T>::type* f, cudaStrea
   return NFFT_SUCCESS;
 }
 
+// pdl: the kernel right before on `st` is this plan's inverse FFT (nfft_adjoint, nfft_execute): the
+// crop launches programmatically (its launch overlaps the FFT's tail) and waits for the grid
 template <typename T>
-nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st) {
+nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st, bool pdl = false) {
   const Geom& g = p->geom;
   if (p->cellmode) {  // the cell-mode spread rewrites every cell: crop only, no re-zeroing
     const int nl = g.N[g.D - 1];
@@ -900,8 +902,10 @@ nfft_status stage_crop(nfft_plan p, typename cplx<T>::type* y, cudaStream_t st) 
     const long long units = rows * ((nl + 1) / 2);
     if (units < (1LL << 31) - THREADS * 4096LL) {  // flattened, two cells per thread
       const unsigned ctas = (unsigned)std::min<long long>((units + THREADS - 1) / THREADS, (long long)p->sm_count * 16);
-      correct_flat_kernel<T, false><<<ctas, THREADS, 0, st>>>(g, (const typename cplx<T>::type*)p->d_grid_adj,
-                                                              (const T*)p->d_betaT, y);
+      using C = typename cplx<T>::type;
+      const void* fn = (const void*)correct_flat_kernel<T, false>;
+      CK((pdl ? launch_k_pdl<Geom, const C*, const T*, C*> : launch_k<Geom, const C*, const T*, C*>)(
+          fn, dim3(ctas), dim3(THREADS), 0, st, g, (const C*)p->d_grid_adj, (const T*)p->d_betaT, y));
     } else {
       dim3 grid((unsigned)std::min<long long>((nl + THREADS - 1) / THREADS, 4096), (unsigned)std::min<long long>(rows, 65535));
       crop_kernel<T><<<grid, THREADS, 0, st>>>(g, (const typename cplx<T>::type*)p->d_grid_adj, (const T*)p->d_betaT, y);
@@ -977,7 +981,7 @@ nfft_status adjoint_impl(nfft_plan p, const void* f_in, void* y_out) {
   rec(p, 1, 2);
   TRY(stage_fft<T>(p, CUFFT_INVERSE, p->stream));
   rec(p, 1, 3);
-  TRY(stage_crop<T>(p, y, p->stream));
+  TRY(stage_crop<T>(p, y, p->stream, true));
   rec(p, 1, 4);
   if (host_out) {
     CK(cudaMemcpyAsync(y_out, y, grid_bytes_out, cudaMemcpyDeviceToHost, p->stream));
@@ -1048,7 +1052,7 @@ nfft_status execute_impl(nfft_plan p, int flags, const void* fhat, void* f_out, 
     if (pre) CK(cudaStreamWaitEvent(p->side_adj, p->ev_pre, 0));
     TRY(stage_spread<T>(p, (const C*)f_in, p->side_adj, fwd));
     TRY(stage_fft<T>(p, CUFFT_INVERSE, p->side_adj));
-    TRY(stage_crop<T>(p, (C*)y_out, p->side_adj));
+    TRY(stage_crop<T>(p, (C*)y_out, p->side_adj, true));
     if (h_y) CK(cudaMemcpyAsync(host_y, y_out, gbytes, cudaMemcpyDeviceToHost, p->side_adj));
     CK(cudaEventRecord(p->ev_adj, p->side_adj));
   }
